@@ -1,0 +1,174 @@
+"""ctypes wrappers around ``sten_oracle.c`` plus a tiny pure-Python brute force.
+
+TEST INFRASTRUCTURE ONLY (see ``oracle/__init__.py``).
+
+Arrays are numpy: fp32 -> ``np.float32``; bf16 -> ``np.uint16`` bit patterns.
+All functions return freshly allocated numpy arrays; nothing is cached.
+"""
+from __future__ import annotations
+
+import ctypes
+import itertools
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sten_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_i64 = ctypes.c_int64
+_ptr = ctypes.c_void_p
+
+
+def lib_path() -> str:
+    return _LIB
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with plain gcc (no fast-math, no FP contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + ".tmp.%d" % os.getpid()
+        subprocess.check_call([
+            "gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+            "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        lib.oracle_sparsify.argtypes = [ctypes.c_int] * 4 + [_ptr, _i64, _i64, _i64, _ptr, _ptr]
+        lib.oracle_densify.argtypes = [ctypes.c_int] * 4 + [_ptr, _ptr, _i64, _i64, _ptr, _i64]
+        lib.oracle_spmm.argtypes = ([ctypes.c_int] * 4 + [_ptr, _ptr, _i64, _i64, _ptr, _i64, _i64,
+                                                          _i64, _i64, _ptr, _ptr, ctypes.c_int])
+        lib.oracle_dense_matmul.argtypes = [ctypes.c_int, _ptr, _i64, _i64, _i64, _ptr, _i64, _i64,
+                                            _ptr, ctypes.c_int]
+        lib.oracle_energy.argtypes = [ctypes.c_int, _ptr, _ptr, _i64, _i64, _i64]
+        lib.oracle_energy.restype = ctypes.c_double
+        for f in (lib.oracle_sparsify, lib.oracle_densify, lib.oracle_spmm, lib.oracle_dense_matmul):
+            f.restype = ctypes.c_int
+        lib.oracle_max_threads.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _dtype_code(a: np.ndarray) -> int:
+    if a.dtype == np.float32:
+        return 0
+    if a.dtype == np.uint16:
+        return 1
+    raise TypeError("oracle arrays must be float32 or uint16 (bf16 bits), got %s" % a.dtype)
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise ValueError("%s failed with oracle status %d" % (what, rc))
+
+
+def max_threads() -> int:
+    return int(_load().oracle_max_threads())
+
+
+def sparsify(W: np.ndarray, n: int, m: int, g: int):
+    """Return (values [M][K/m*n], idx [M/g][K/m][n] uint8) for a dense W [M][K]."""
+    W = np.ascontiguousarray(W)
+    M, K = W.shape
+    dt = _dtype_code(W)
+    if M % g or K % m:
+        raise ValueError("shape (%d, %d) not divisible by g=%d / m=%d" % (M, K, g, m))
+    values = np.zeros((M, K // m * n), dtype=W.dtype)
+    idx = np.zeros((M // g, K // m, n), dtype=np.uint8)
+    _check(_load().oracle_sparsify(n, m, g, dt, _p(W), M, K, K, _p(values), _p(idx)), "sparsify")
+    return values, idx
+
+
+def densify(values: np.ndarray, idx: np.ndarray, n: int, m: int, g: int, K: int) -> np.ndarray:
+    values = np.ascontiguousarray(values)
+    idx = np.ascontiguousarray(idx, dtype=np.uint8)
+    M = values.shape[0]
+    out = np.empty((M, K), dtype=values.dtype)
+    _check(_load().oracle_densify(n, m, g, _dtype_code(values), _p(values), _p(idx), M, K,
+                                  _p(out), K), "densify")
+    return out
+
+
+def spmm(values: np.ndarray, idx: np.ndarray, B: np.ndarray, n: int, m: int, g: int,
+         cols: tuple | None = None, nthreads: int = 1, with_bound: bool = True):
+    """fp64 reference C = mask(W) @ B (and Bound = |mask(W)| @ |B|).
+
+    ``cols=(c0, c1)`` restricts the computation to a column slice; the
+    returned arrays are then [M][c1-c0].
+    """
+    values = np.ascontiguousarray(values)
+    idx = np.ascontiguousarray(idx, dtype=np.uint8)
+    B = np.ascontiguousarray(B)
+    if B.dtype != values.dtype:
+        raise TypeError("values and B must share a dtype")
+    M = values.shape[0]
+    K, N = B.shape
+    c0, c1 = (0, N) if cols is None else cols
+    C = np.zeros((M, N), dtype=np.float64)
+    Bd = np.zeros_like(C) if with_bound else None
+    _check(_load().oracle_spmm(n, m, g, _dtype_code(values), _p(values), _p(idx), M, K, _p(B), N,
+                               N, c0, c1, _p(C), _p(Bd) if with_bound else None, nthreads), "spmm")
+    if cols is not None:
+        C = C[:, c0:c1].copy()
+        Bd = Bd[:, c0:c1].copy() if with_bound else None
+    return (C, Bd) if with_bound else C
+
+
+def dense_matmul(A: np.ndarray, B: np.ndarray, nthreads: int = 1) -> np.ndarray:
+    A = np.ascontiguousarray(A)
+    B = np.ascontiguousarray(B)
+    M, K = A.shape
+    K2, N = B.shape
+    assert K == K2 and A.dtype == B.dtype
+    C = np.empty((M, N), dtype=np.float64)
+    _check(_load().oracle_dense_matmul(_dtype_code(A), _p(A), M, K, K, _p(B), N, N, _p(C), nthreads),
+           "dense_matmul")
+    return C
+
+
+def energy(Xhat: np.ndarray, X: np.ndarray) -> float:
+    """||X^||_1 / ||X||_1."""
+    Xhat = np.ascontiguousarray(Xhat)
+    X = np.ascontiguousarray(X)
+    assert Xhat.shape == X.shape and Xhat.dtype == X.dtype
+    M, K = X.shape
+    return float(_load().oracle_energy(_dtype_code(X), _p(Xhat), _p(X), M, K, K))
+
+
+def brute_select(W_int: np.ndarray, n: int, m: int, g: int) -> np.ndarray:
+    """Exhaustive selection for tiny integer-valued W (pure Python).
+
+    For every (group, m-block) enumerate all C(m, n) position subsets, sum the
+    exact |w| of the group's rows over each subset in fp64 (exact for small
+    integers), and keep the subset with the largest sum -- the argmax of the L1
+    objective restricted to one group/block.  Ties go to the
+    lexicographically smallest sorted subset.  Returns idx [M/g][K/m][n].
+    """
+    W = np.asarray(W_int, dtype=np.float64)
+    M, K = W.shape
+    G, KB = M // g, K // m
+    out = np.zeros((G, KB, n), dtype=np.uint8)
+    for grp in range(G):
+        rows = W[grp * g:(grp + 1) * g]
+        for kb in range(KB):
+            blk = np.abs(rows[:, kb * m:(kb + 1) * m])
+            best, best_sum = None, -1.0
+            for subset in itertools.combinations(range(m), n):  # lexicographic order
+                tot = float(sum(blk[i][j] for i in range(g) for j in subset))
+                if tot > best_sum:
+                    best, best_sum = subset, tot
+            out[grp, kb] = best
+    return out

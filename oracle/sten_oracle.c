@@ -1,0 +1,226 @@
+/*
+ * sten_oracle.c -- plain, slow, obviously-correct CPU ORACLE for the grouped
+ * n:m layout of STen (arXiv 2304.07613).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header, table or helper with the CUDA path
+ * (paper_2304_07613_b200/csrc); neither side includes the other.
+ *
+ * Reading of the paper followed here:
+ *   - n:m: "each group of m elements has n nonzeros"
+ *   - group: "each nonzero pattern is repeated g times,
+ *     forming a group"
+ *     -> reading (A) free grouping: g consecutive rows share one n-of-m pattern
+ *        per m-block along K (the contraction axis).
+ *   - objective: argmax ||X^|| with the L1 norm
+ *     -> for (A) the argmax decomposes per (group, m-block): keep the n
+ *        positions with the largest summed |w| over the group's g rows.
+ *   - densify: "a single iteration over the values, reordering their
+ *     location according to the stored index"
+ *   - product: the sparse-dense GEMM C = A_sparse * B
+ *
+ * Arithmetic readings (paper silent; readings R4, R5, R10):
+ *   - score s[j] = fl32(...fl32(|w[r0][j]| + |w[r0+1][j]|) ... + |w[r0+g-1][j]|),
+ *     fp32, rows in ascending order, round-to-nearest-even, adds only.
+ *     (built with -ffp-contract=off; there are no multiplies anyway)
+ *   - rank[j] = #{ i : s[i] > s[j]  or  (s[i] == s[j] and i < j) };
+ *     keep j iff rank[j] < n; idx lists kept j ascending.
+ *   - SpMM reference in fp64, ascending k; Bound = sum |v|*|b| in fp64.
+ *
+ * Element types: dtype 0 = fp32, dtype 1 = bf16 stored as uint16 bit
+ * patterns; bf16 is widened to fp32 exactly (bits << 16).
+ *
+ * Layouts (same logical layout as include/sten.h, written out independently):
+ *   W      [M][ldw]            row-major, K <= ldw
+ *   values [M][K/m*n]          row-major; values[r][kb*n+t]
+ *   idx    [M/g][K/m][n]       uint8, ascending within each (group, block)
+ *   B      [K][ldb]            row-major, N <= ldb
+ *   C, Bound [M][N] (double)   row-major, only columns [c0, c1) written
+ *
+ * Parity status: every function here is pinned by tests/test_oracle_pins.py
+ * (brute force over all C(m,n) subsets, textbook per-block top-n at g=1,
+ * SPEC.md examples, closed forms B = I, integer-exact masked dense product,
+ * energy inequalities).  No function is "parity unpinned".
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static float widen(int dtype, const void* base, int64_t i)
+{
+    if (dtype == 0) return ((const float*)base)[i];
+    uint32_t bits = (uint32_t)((const uint16_t*)base)[i] << 16;
+    float f;
+    memcpy(&f, &bits, sizeof f);
+    return f;
+}
+
+static void copy_elem(int dtype, void* dst, int64_t di, const void* src, int64_t si)
+{
+    if (dtype == 0) ((float*)dst)[di] = ((const float*)src)[si];
+    else ((uint16_t*)dst)[di] = ((const uint16_t*)src)[si];
+}
+
+static void zero_elem(int dtype, void* dst, int64_t di)
+{
+    if (dtype == 0) ((float*)dst)[di] = 0.0f;
+    else ((uint16_t*)dst)[di] = 0;
+}
+
+static int check_args(int n, int m, int g, int dtype, int64_t M, int64_t K)
+{
+    if (n < 1 || m > 16 || n >= m || g < 1) return 1;
+    if (dtype != 0 && dtype != 1) return 1;
+    if (M < 0 || K < 0) return 1;
+    if (M % g != 0 || K % m != 0) return 2;
+    return 0;
+}
+
+/* a1-a3: magnitude sparsifier to grouped n:m (reading A). */
+int oracle_sparsify(int n, int m, int g, int dtype,
+                    const void* W, int64_t M, int64_t K, int64_t ldw,
+                    void* values, uint8_t* idx)
+{
+    int rc = check_args(n, m, g, dtype, M, K);
+    if (rc) return rc;
+    if (ldw < K) return 2;
+    int64_t KB = K / m, Kp = KB * n, G = M / g;
+    for (int64_t grp = 0; grp < G; ++grp) {
+        for (int64_t kb = 0; kb < KB; ++kb) {
+            float s[16];
+            /* score: L1 magnitude of each in-block position over the group's rows */
+            for (int j = 0; j < m; ++j) {
+                float acc = 0.0f;
+                for (int i = 0; i < g; ++i) {
+                    int64_t r = grp * g + i;
+                    acc = acc + fabsf(widen(dtype, W, r * ldw + kb * m + j));
+                }
+                s[j] = acc;
+            }
+            /* select: rank rule (larger score first, lower position on ties) */
+            int t = 0;
+            for (int j = 0; j < m; ++j) {
+                int rank = 0;
+                for (int i = 0; i < m; ++i)
+                    if (s[i] > s[j] || (s[i] == s[j] && i < j)) rank++;
+                if (rank < n) {
+                    idx[(grp * KB + kb) * n + t] = (uint8_t)j;
+                    t++;
+                }
+            }
+            /* compact: bit copy of the kept weights of every row of the group */
+            for (int i = 0; i < g; ++i) {
+                int64_t r = grp * g + i;
+                for (int u = 0; u < n; ++u) {
+                    int j = idx[(grp * KB + kb) * n + u];
+                    copy_elem(dtype, values, r * Kp + kb * n + u, W, r * ldw + kb * m + j);
+                }
+            }
+        }
+    }
+    return 0;
+}
+
+/* a4: densify -- zero-fill, then scatter each stored value to its position. */
+int oracle_densify(int n, int m, int g, int dtype,
+                   const void* values, const uint8_t* idx, int64_t M, int64_t K,
+                   void* W_out, int64_t ldw)
+{
+    int rc = check_args(n, m, g, dtype, M, K);
+    if (rc) return rc;
+    if (ldw < K) return 2;
+    int64_t KB = K / m, Kp = KB * n;
+    for (int64_t r = 0; r < M; ++r)
+        for (int64_t k = 0; k < K; ++k)
+            zero_elem(dtype, W_out, r * ldw + k);
+    for (int64_t r = 0; r < M; ++r) {
+        int64_t grp = r / g;
+        for (int64_t kb = 0; kb < KB; ++kb)
+            for (int u = 0; u < n; ++u) {
+                int j = idx[(grp * KB + kb) * n + u];
+                copy_elem(dtype, W_out, r * ldw + kb * m + j, values, r * Kp + kb * n + u);
+            }
+    }
+    return 0;
+}
+
+/* a5-a7: C[r][c] = sum_{kb,t} values[r][kb*n+t] * B[kb*m + idx][c]   (fp64,
+ * ascending k), and Bound[r][c] = sum |values| * |B|.  Columns [c0, c1). */
+int oracle_spmm(int n, int m, int g, int dtype,
+                const void* values, const uint8_t* idx, int64_t M, int64_t K,
+                const void* B, int64_t ldb, int64_t N, int64_t c0, int64_t c1,
+                double* C, double* Bound, int nthreads)
+{
+    int rc = check_args(n, m, g, dtype, M, K);
+    if (rc) return rc;
+    if (ldb < N || c0 < 0 || c1 > N || c0 > c1) return 2;
+    int64_t KB = K / m, Kp = KB * n;
+#ifdef _OPENMP
+    if (nthreads < 1) nthreads = 1;
+#pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1)
+#endif
+    for (int64_t r = 0; r < M; ++r) {
+        int64_t grp = r / g;
+        for (int64_t c = c0; c < c1; ++c) {
+            double acc = 0.0, bound = 0.0;
+            for (int64_t kb = 0; kb < KB; ++kb)
+                for (int u = 0; u < n; ++u) {
+                    int64_t k = kb * m + idx[(grp * KB + kb) * n + u];
+                    double v = (double)widen(dtype, values, r * Kp + kb * n + u);
+                    double b = (double)widen(dtype, B, k * ldb + c);
+                    acc += v * b;
+                    bound += fabs(v) * fabs(b);
+                }
+            C[r * N + c] = acc;
+            if (Bound) Bound[r * N + c] = bound;
+        }
+    }
+    return 0;
+}
+
+/* Independent second path for the product: naive fp64 triple loop over a
+ * dense (already masked) A[M][lda] times B[K][ldb]. */
+int oracle_dense_matmul(int dtype, const void* A, int64_t M, int64_t K, int64_t lda,
+                        const void* B, int64_t ldb, int64_t N, double* C, int nthreads)
+{
+    if (lda < K || ldb < N) return 2;
+#ifdef _OPENMP
+    if (nthreads < 1) nthreads = 1;
+#pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1)
+#endif
+    for (int64_t r = 0; r < M; ++r)
+        for (int64_t c = 0; c < N; ++c) {
+            double acc = 0.0;
+            for (int64_t k = 0; k < K; ++k)
+                acc += (double)widen(dtype, A, r * lda + k) * (double)widen(dtype, B, k * ldb + c);
+            C[r * N + c] = acc;
+        }
+    return 0;
+}
+
+/* energy = ||X^||_1 / ||X||_1, fp64. */
+double oracle_energy(int dtype, const void* Xhat, const void* X, int64_t M, int64_t K, int64_t ld)
+{
+    double num = 0.0, den = 0.0;
+    for (int64_t r = 0; r < M; ++r)
+        for (int64_t k = 0; k < K; ++k) {
+            num += fabs((double)widen(dtype, Xhat, r * ld + k));
+            den += fabs((double)widen(dtype, X, r * ld + k));
+        }
+    return den > 0.0 ? num / den : 0.0;
+}
+
+int oracle_max_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
