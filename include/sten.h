@@ -1,0 +1,157 @@
+/*
+ * sten.h -- C ABI of the B200-native grouped n:m hot path of STen
+ * (arXiv 2304.07613, Sec. 5 "Grouped n:m Sparsity").
+ *
+ * The library (paper_2304_07613_b200/libsten.so) exports exactly the
+ * functions declared here.  No torch / CUDA types appear in the signatures:
+ * a stream is passed as an opaque `void*` holding a cudaStream_t (NULL = the
+ * legacy default stream).
+ *
+ * ---------------------------------------------------------------------------
+ * The layout (reading (A) "free grouping", R1/R2):
+ *   W  is M x K (M = output features = group axis, K = input features =
+ *      sparse / contraction axis).  K is cut into K/m blocks of m consecutive
+ *      elements ("each group of m elements has n nonzeros").
+ *   g consecutive rows form a group that shares ONE n-of-m pattern per block
+ *   ("each nonzero pattern is repeated g times, forming a group",
+ *   PAPER.md:518).  Kept positions maximise the L1 norm of the kept entries
+ *   (PAPER.md:548-549): per (group, block) the n positions with the largest
+ *   score s[j] = sum_{i<g} |w[group*g+i][block*m+j]| are kept.
+ *
+ *   values [M][K/m*n]       row-major, element type = the W dtype;
+ *                           values[r][kb*n+t] = W[r][kb*m + idx[r/g][kb][t]]
+ *   idx    [M/g][K/m][n]    uint8, in-block positions, strictly ascending
+ *
+ * Arithmetic contract (R4, R5, R10):
+ *   - scores are fp32 sums of |w| over the group's rows in ascending row
+ *     order, round-to-nearest-even, no contraction; bf16 inputs are widened
+ *     exactly; ties go to the lower in-block position;
+ *   - exactly n entries are stored per (row, block), even if some are zero;
+ *   - SpMM accumulates in fp32; the per-column summation order depends only
+ *     on (M, K, n, m, g) and the plan, never on N or on the column tiling, so
+ *     a column-sharded product equals the unsharded one bit for bit when both
+ *     use the same plan (sten_spmm_plan_query on the global shape).
+ *
+ * Conventions for every entry point:
+ *   - Pointers are DEVICE pointers of the current device unless the name ends
+ *     in _host.  The caller allocates every buffer; the library allocates no
+ *     persistent memory, keeps no global state and is safe to call
+ *     concurrently on different streams / devices.
+ *   - Work is enqueued asynchronously on `stream` (except the _host calls,
+ *     which return after the stream has drained).
+ *   - Argument errors are detected synchronously BEFORE any launch, so an
+ *     error return leaves every output untouched:
+ *        NULL pointer, n/m/g out of range, unknown dtype  -> STEN_ERR_INVALID_ARG
+ *        M % g != 0, K % m != 0, ld < extent, negative size -> STEN_ERR_SHAPE
+ *        no compiled variant / misaligned vector pointer or ld
+ *          (16-byte base alignment; fp32 ld % 4, bf16 ld % 8)  -> STEN_ERR_UNSUPPORTED
+ *        a CUDA launch / copy error                        -> STEN_ERR_CUDA
+ *     There is no CPU fallback: without a usable device the calls fail.
+ *   - Outputs must not overlap inputs.
+ *   - Supported formats: 1 <= n < m <= 16 with m in {2,4,6,8,10,12,16};
+ *     any g >= 1 with g | M.  Empty problems (M, K or N == 0) are valid
+ *     no-ops apart from zero-filling outputs whose value is defined
+ *     (C = 0 when K == 0).
+ */
+#ifndef STEN_H_
+#define STEN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    STEN_OK = 0,
+    STEN_ERR_INVALID_ARG = 1,
+    STEN_ERR_SHAPE = 2,
+    STEN_ERR_UNSUPPORTED = 3,
+    STEN_ERR_CUDA = 4
+} sten_status;
+
+typedef enum { STEN_F32 = 0, STEN_BF16 = 1 } sten_dtype;
+
+/* n kept of every m consecutive K elements; g rows per group. */
+typedef struct { int32_t n, m, g; } sten_nmg;
+
+/* SpMM kernel families (sten_spmm_plan.algo). */
+typedef enum {
+    STEN_ALGO_AUTO = 0,       /* library chooses                                    */
+    STEN_ALGO_SIMT = 1,       /* CUDA-core FFMA, fp32 accumulate (fp32 or bf16 in)  */
+    STEN_ALGO_MMA_SYNC = 2,   /* bf16 warp-level mma.sync on gathered rows          */
+    STEN_ALGO_TCGEN05 = 3     /* bf16 tcgen05 / TMEM on gathered dense sub-tiles    */
+} sten_algo;
+
+/* Execution plan of one SpMM.  split_k = number of K partitions reduced in a
+ * fixed order (1 = none); tile = kernel tile variant of the algorithm (0 =
+ * library choice; see DESIGN.md for the table).  Fields are filled by
+ * sten_spmm_plan_query; a caller may override them (a value out of range or a
+ * variant not compiled for this g -> STEN_ERR_UNSUPPORTED). */
+typedef struct {
+    int32_t algo;
+    int32_t split_k;
+    int32_t tile;
+    int32_t reserved[5];
+} sten_spmm_plan;
+
+/* a1-a3: magnitude sparsifier dense -> grouped n:m.
+ *   W      [M][ldw] dtype dt, K <= ldw                      (input)
+ *   values [M][K/m*n] dtype dt                              (output, overwritten)
+ *   idx    [M/g][K/m][n] uint8                              (output, overwritten) */
+sten_status sten_sparsify_grouped_nm(sten_nmg f, sten_dtype dt,
+                                     const void* W, int64_t M, int64_t K, int64_t ldw,
+                                     void* values, uint8_t* idx, void* stream);
+
+/* a4: grouped n:m -> dense.  W_out [M][ldw] receives zeros at
+ * pruned positions and the stored values at kept ones (columns >= K untouched). */
+sten_status sten_densify(sten_nmg f, sten_dtype dt,
+                         const void* values, const uint8_t* idx, int64_t M, int64_t K,
+                         void* W_out, int64_t ldw, void* stream);
+
+/* a5-a7 (Fig. 5): C = densify(values, idx) x B.
+ *   values/idx as produced by sten_sparsify_grouped_nm, element type ab_dt
+ *   B [K][ldb] ab_dt, N <= ldb       C [M][ldc] c_dt, N <= ldc, overwritten (beta = 0) */
+sten_status sten_spmm_grouped_nm(sten_nmg f, sten_dtype ab_dt,
+                                 const void* values, const uint8_t* idx, int64_t M, int64_t K,
+                                 const void* B, int64_t ldb, int64_t N,
+                                 void* C, int64_t ldc, sten_dtype c_dt, void* stream);
+
+/* The plan sten_spmm_grouped_nm would use for this problem. */
+sten_status sten_spmm_plan_query(sten_nmg f, sten_dtype ab_dt, int64_t M, int64_t K, int64_t N,
+                                 sten_dtype c_dt, sten_spmm_plan* plan);
+
+/* sten_spmm_grouped_nm with an explicit plan (NULL = AUTO). */
+sten_status sten_spmm_grouped_nm_ex(sten_nmg f, sten_dtype ab_dt,
+                                    const void* values, const uint8_t* idx, int64_t M, int64_t K,
+                                    const void* B, int64_t ldb, int64_t N,
+                                    void* C, int64_t ldc, sten_dtype c_dt,
+                                    const sten_spmm_plan* plan, void* stream);
+
+/* End-to-end sparse linear layer with HOST input/output buffers: copies
+ * W_host [M][ldw] and B_host [K][ldb] to the device, sparsifies W, multiplies,
+ * copies C back to C_host [M][ldc] and waits for the stream.  Host buffers
+ * should be pinned (cudaHostAlloc / torch pin_memory) for asynchronous copies.
+ * `workspace` is a device buffer of at least
+ * sten_sparse_linear_host_workspace_size(...) bytes (16-byte aligned). */
+int64_t sten_sparse_linear_host_workspace_size(sten_nmg f, sten_dtype ab_dt, int64_t M,
+                                               int64_t K, int64_t N, sten_dtype c_dt);
+sten_status sten_sparse_linear_host(sten_nmg f, sten_dtype ab_dt,
+                                    const void* W_host, int64_t M, int64_t K, int64_t ldw,
+                                    const void* B_host, int64_t ldb, int64_t N,
+                                    void* C_host, int64_t ldc, sten_dtype c_dt,
+                                    void* workspace, int64_t workspace_bytes, void* stream);
+
+const char* sten_status_string(sten_status s);
+const char* sten_algo_name(int32_t algo);
+/* Number of kernel launches the last call of each entry point enqueues is
+ * deterministic; this returns the count for one sten_spmm_grouped_nm_ex call
+ * with `plan` (used by bench.py's gpu_launches accounting). */
+int32_t sten_spmm_launch_count(const sten_spmm_plan* plan);
+int32_t sten_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STEN_H_ */

@@ -1,0 +1,428 @@
+// sten_api.cu -- the C ABI declared in include/sten.h: argument validation,
+// plan selection, kernel instantiation and launch on the caller's stream.
+#include "sten.h"
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "sparsify.cuh"
+#include "spmm_simt.cuh"
+#include "spmm_mma.cuh"
+
+using namespace sten;
+
+namespace {
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline size_t dt_size(sten_dtype d) { return d == STEN_F32 ? 4 : 2; }
+
+inline bool dtype_ok(int d) { return d == STEN_F32 || d == STEN_BF16; }
+
+inline bool m_supported(int m) {
+    return m == 2 || m == 4 || m == 6 || m == 8 || m == 10 || m == 12 || m == 16;
+}
+
+sten_status check_format(sten_nmg f) {
+    if (f.n < 1 || f.m > 16 || f.n >= f.m || f.g < 1) return STEN_ERR_INVALID_ARG;
+    if (!m_supported(f.m)) return STEN_ERR_UNSUPPORTED;
+    return STEN_OK;
+}
+
+sten_status check_shape(sten_nmg f, int64_t M, int64_t K) {
+    if (M < 0 || K < 0) return STEN_ERR_SHAPE;
+    if (M % f.g != 0 || K % f.m != 0) return STEN_ERR_SHAPE;
+    return STEN_OK;
+}
+
+inline sten_status last_cuda() {
+    return cudaGetLastError() == cudaSuccess ? STEN_OK : STEN_ERR_CUDA;
+}
+
+inline unsigned grid1d(int64_t threads) { return unsigned((threads + 255) / 256); }
+
+// ---------------------------------------------------------------------------------------------
+// K1 / K2 dispatch on (dtype, m)
+// ---------------------------------------------------------------------------------------------
+template <typename T, int MB>
+void launch_sparsify(const void* W, int64_t ldw, int64_t G, int64_t KB, sten_nmg f, void* values,
+                     int64_t Kp, uint8_t* idx, bool aligned, cudaStream_t st) {
+    sparsify_grouped_nm_kernel<T, MB><<<grid1d(G * KB), 256, 0, st>>>(
+        static_cast<const T*>(W), ldw, G, KB, f.n, f.g, static_cast<T*>(values), Kp, idx, aligned);
+}
+
+template <typename T>
+bool dispatch_sparsify(int m, const void* W, int64_t ldw, int64_t G, int64_t KB, sten_nmg f,
+                       void* values, int64_t Kp, uint8_t* idx, bool aligned, cudaStream_t st) {
+    switch (m) {
+        case 2: launch_sparsify<T, 2>(W, ldw, G, KB, f, values, Kp, idx, aligned, st); return true;
+        case 4: launch_sparsify<T, 4>(W, ldw, G, KB, f, values, Kp, idx, aligned, st); return true;
+        case 6: launch_sparsify<T, 6>(W, ldw, G, KB, f, values, Kp, idx, aligned, st); return true;
+        case 8: launch_sparsify<T, 8>(W, ldw, G, KB, f, values, Kp, idx, aligned, st); return true;
+        case 10: launch_sparsify<T, 10>(W, ldw, G, KB, f, values, Kp, idx, aligned, st); return true;
+        case 12: launch_sparsify<T, 12>(W, ldw, G, KB, f, values, Kp, idx, aligned, st); return true;
+        case 16: launch_sparsify<T, 16>(W, ldw, G, KB, f, values, Kp, idx, aligned, st); return true;
+    }
+    return false;
+}
+
+template <typename T, int MB>
+void launch_densify(const void* values, const uint8_t* idx, int64_t M, int64_t KB, sten_nmg f,
+                    int64_t Kp, void* W, int64_t ldw, bool aligned, cudaStream_t st) {
+    densify_grouped_nm_kernel<T, MB><<<grid1d(M * KB), 256, 0, st>>>(
+        static_cast<const T*>(values), idx, M, KB, f.n, f.g, Kp, static_cast<T*>(W), ldw, aligned);
+}
+
+template <typename T>
+bool dispatch_densify(int m, const void* values, const uint8_t* idx, int64_t M, int64_t KB,
+                      sten_nmg f, int64_t Kp, void* W, int64_t ldw, bool aligned, cudaStream_t st) {
+    switch (m) {
+        case 2: launch_densify<T, 2>(values, idx, M, KB, f, Kp, W, ldw, aligned, st); return true;
+        case 4: launch_densify<T, 4>(values, idx, M, KB, f, Kp, W, ldw, aligned, st); return true;
+        case 6: launch_densify<T, 6>(values, idx, M, KB, f, Kp, W, ldw, aligned, st); return true;
+        case 8: launch_densify<T, 8>(values, idx, M, KB, f, Kp, W, ldw, aligned, st); return true;
+        case 10: launch_densify<T, 10>(values, idx, M, KB, f, Kp, W, ldw, aligned, st); return true;
+        case 12: launch_densify<T, 12>(values, idx, M, KB, f, Kp, W, ldw, aligned, st); return true;
+        case 16: launch_densify<T, 16>(values, idx, M, KB, f, Kp, W, ldw, aligned, st); return true;
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------------------------------------
+// SpMM dispatch
+// ---------------------------------------------------------------------------------------------
+int simt_rows_per_warp(int g) {
+    if (g % 8 == 0) return 8;
+    if (g % 4 == 0) return 4;
+    if (g % 2 == 0) return 2;
+    return 1;
+}
+
+// SIMT tile variants (plan.tile): 1 = TN8/SUB1, 2 = TN8/SUB2, 3 = TN8/SUB4, 4 = TN4/SUB8.
+struct SimtTile { int tn, sub; };
+constexpr SimtTile kSimtTiles[5] = {{0, 0}, {8, 1}, {8, 2}, {8, 4}, {4, 8}};
+
+inline bool simt_tile_ok(int tile, int rg) {
+    if (tile < 1 || tile > 4) return false;
+    return rg * kSimtTiles[tile].tn * kSimtTiles[tile].sub <= 128;    // accumulators per lane
+}
+
+template <typename TAB, typename TC, int RG, int TN, int SUB>
+sten_status launch_simt_cfg(const SpmmArgs& a, int split, cudaStream_t st) {
+    if constexpr (RG * TN * SUB > 128 || TN < 16 / int(sizeof(TAB))) {
+        return STEN_ERR_UNSUPPORTED;
+    } else {
+        using Cfg = SimtCfg<TAB, RG, TN, SUB>;
+        const size_t smem = simt_smem_bytes<TAB, RG, TN, SUB>(a.m);
+        auto kern = spmm_simt_kernel<TAB, TC, RG, TN, SUB>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+            return STEN_ERR_CUDA;
+        dim3 grid(unsigned((a.N + Cfg::kBN - 1) / Cfg::kBN), unsigned((a.M + Cfg::kBM - 1) / Cfg::kBM),
+                  unsigned(split));
+        kern<<<grid, Cfg::kThreads, smem, st>>>(a);
+        return last_cuda();
+    }
+}
+
+template <typename TAB, typename TC, int RG>
+sten_status launch_simt_rg(const SpmmArgs& a, int tile, int split, cudaStream_t st) {
+    switch (tile) {
+        case 1: return launch_simt_cfg<TAB, TC, RG, 8, 1>(a, split, st);
+        case 2: return launch_simt_cfg<TAB, TC, RG, 8, 2>(a, split, st);
+        case 3: return launch_simt_cfg<TAB, TC, RG, 8, 4>(a, split, st);
+        case 4: return launch_simt_cfg<TAB, TC, RG, 4, 8>(a, split, st);
+    }
+    return STEN_ERR_UNSUPPORTED;
+}
+
+template <typename TAB, typename TC>
+sten_status launch_simt(const SpmmArgs& a, int tile, int split, cudaStream_t st) {
+    switch (simt_rows_per_warp(a.g)) {
+        case 8: return launch_simt_rg<TAB, TC, 8>(a, tile, split, st);
+        case 4: return launch_simt_rg<TAB, TC, 4>(a, tile, split, st);
+        case 2: return launch_simt_rg<TAB, TC, 2>(a, tile, split, st);
+        default: return launch_simt_rg<TAB, TC, 1>(a, tile, split, st);
+    }
+}
+
+template <typename TC>
+sten_status launch_reduce(const float* parts, int split, int64_t M, int64_t N, void* C, int64_t ldc,
+                          cudaStream_t st) {
+    splitk_reduce_kernel<TC><<<grid1d(M * N), 256, 0, st>>>(parts, split, M, N, static_cast<TC*>(C), ldc);
+    return last_cuda();
+}
+
+template <typename TC>
+__global__ void zero_fill_kernel(TC* C, int64_t M, int64_t N, int64_t ldc) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= M * N) return;
+    const int64_t r = i / N, c = i - r * N;
+    C[r * ldc + c] = TC(0);
+}
+
+constexpr int kNumSMs = 148;
+
+// Pick split_k for `tiles` output tiles over KB m-blocks: minimise
+// waves(S) * ceil(KB/S) * t_kb + reduce(S), with one resident CTA per SM.
+int choose_split(int64_t tiles, int64_t KB, double t_kb_clk, double reduce_clk_per_split) {
+    int best = 1;
+    double best_t = 1e300;
+    for (int S = 1; S <= 16 && S <= KB; ++S) {
+        const double waves = double((tiles * S + kNumSMs - 1) / kNumSMs);
+        const double t = waves * double((KB + S - 1) / S) * t_kb_clk + (S > 1 ? S * reduce_clk_per_split : 0.0);
+        if (t < best_t * 0.97) { best_t = t; best = S; }
+    }
+    return best;
+}
+
+sten_status plan_auto(sten_nmg f, sten_dtype ab, int64_t M, int64_t K, int64_t N, sten_dtype c,
+                      sten_spmm_plan* p) {
+    (void)c;
+    memset(p, 0, sizeof(*p));
+    const int64_t KB = K / f.m;
+    const double d = double(f.n) / f.m;
+    if (ab == STEN_BF16 && mma_supported(f.g)) {
+        p->algo = STEN_ALGO_MMA_SYNC;
+        p->tile = f.g % 16 == 0 ? 2 : 1;
+        const int64_t bm = 256, bn = 64;
+        const int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
+        const double t_kb = double(bm * bn * f.n) / 512.0;      // clk per m-block per CTA (MMA-bound guess)
+        const double red = double(M) * N * 8.0 / (kNumSMs * 40.0);
+        p->split_k = choose_split(tiles, KB, t_kb, red);
+        return STEN_OK;
+    }
+    p->algo = STEN_ALGO_SIMT;
+    const int rg = simt_rows_per_warp(f.g);
+    int tile = 1;
+    for (int t = 1; t <= 3; ++t) {
+        if (!simt_tile_ok(t, rg)) break;
+        tile = t;
+        if (8.0 * kSimtTiles[t].sub * rg * d >= 32.0) break;
+    }
+    p->tile = tile;
+    const int64_t bm = 8 * kSimtTiles[tile].sub * rg, bn = 32 * kSimtTiles[tile].tn;
+    const int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
+    const double t_kb = double(bm * bn * f.n) / 128.0;          // clk per m-block per CTA (FFMA-bound)
+    const double red = double(M) * N * 8.0 / (kNumSMs * 40.0);
+    p->split_k = choose_split(tiles, KB, t_kb, red);
+    return STEN_OK;
+}
+
+sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const uint8_t* idx, int64_t M,
+                      int64_t K, const void* B, int64_t ldb, int64_t N, void* C, int64_t ldc,
+                      sten_dtype c_dt, const sten_spmm_plan* plan_in, cudaStream_t st) {
+    sten_status s = check_format(f);
+    if (s) return s;
+    if (!dtype_ok(ab_dt) || !dtype_ok(c_dt)) return STEN_ERR_INVALID_ARG;
+    if ((s = check_shape(f, M, K))) return s;
+    if (N < 0 || ldb < N || ldc < N) return STEN_ERR_SHAPE;
+    // a buffer may be NULL only when it is empty
+    if ((M * K > 0 && (!values || !idx)) || (K * N > 0 && !B) || (M * N > 0 && !C)) return STEN_ERR_INVALID_ARG;
+    const size_t sab = dt_size(ab_dt), sc = dt_size(c_dt);
+    if (K * N > 0 && (!aligned16(B) || (ldb * int64_t(sab)) % 16 != 0)) return STEN_ERR_UNSUPPORTED;
+    sten_spmm_plan plan;
+    plan_auto(f, ab_dt, M, K, N, c_dt, &plan);
+    if (plan_in) {
+        if (plan_in->algo != STEN_ALGO_AUTO && plan_in->algo != plan.algo) {
+            plan.algo = plan_in->algo;
+            plan.tile = plan.algo == STEN_ALGO_SIMT ? 1 : (f.g % 16 == 0 ? 2 : 1);
+        }
+        if (plan_in->tile > 0) plan.tile = plan_in->tile;
+        if (plan_in->split_k > 0) plan.split_k = plan_in->split_k;
+    }
+    if (plan.split_k < 1 || plan.split_k > 64) return STEN_ERR_UNSUPPORTED;
+    if (plan.algo == STEN_ALGO_MMA_SYNC && (ab_dt != STEN_BF16 || !mma_supported(f.g)))
+        return STEN_ERR_UNSUPPORTED;
+    if (plan.algo != STEN_ALGO_SIMT && plan.algo != STEN_ALGO_MMA_SYNC) return STEN_ERR_UNSUPPORTED;
+    if (plan.algo == STEN_ALGO_SIMT && !simt_tile_ok(plan.tile, simt_rows_per_warp(f.g))) return STEN_ERR_UNSUPPORTED;
+    if (plan.algo == STEN_ALGO_MMA_SYNC && !(plan.tile == 1 || (plan.tile == 2 && f.g % 16 == 0)))
+        return STEN_ERR_UNSUPPORTED;
+    if (M == 0 || N == 0) return STEN_OK;
+    if (K == 0) {
+        if (c_dt == STEN_F32) zero_fill_kernel<float><<<grid1d(M * N), 256, 0, st>>>(static_cast<float*>(C), M, N, ldc);
+        else zero_fill_kernel<bf16_t><<<grid1d(M * N), 256, 0, st>>>(static_cast<bf16_t*>(C), M, N, ldc);
+        return last_cuda();
+    }
+
+    SpmmArgs a;
+    a.values = values; a.idx = idx; a.B = B; a.C = C;
+    a.M = M; a.K = K; a.N = N; a.ldb = ldb; a.ldc = ldc;
+    a.n = f.n; a.m = f.m; a.g = f.g;
+    a.KB = K / f.m; a.Kp = a.KB * f.n;
+    const int split = int(plan.split_k > a.KB ? a.KB : plan.split_k);
+    a.kb_per_split = (a.KB + split - 1) / split;
+    a.c_vec = aligned16(C) && (ldc * int64_t(sc)) % 16 == 0;
+
+    float* parts = nullptr;
+    if (split > 1) {
+        if (cudaMallocAsync(reinterpret_cast<void**>(&parts), size_t(split) * M * N * 4, st) != cudaSuccess)
+            return STEN_ERR_CUDA;
+        a.C = parts;
+    }
+    if (plan.algo == STEN_ALGO_SIMT) {
+        if (ab_dt == STEN_F32) s = c_dt == STEN_F32 ? launch_simt<float, float>(a, plan.tile, split, st)
+                                                    : launch_simt<float, bf16_t>(a, plan.tile, split, st);
+        else s = c_dt == STEN_F32 ? launch_simt<bf16_t, float>(a, plan.tile, split, st)
+                                  : launch_simt<bf16_t, bf16_t>(a, plan.tile, split, st);
+    } else {
+        s = c_dt == STEN_F32 ? launch_mma<float>(a, plan.tile, split, st) : launch_mma<bf16_t>(a, plan.tile, split, st);
+    }
+    if (split > 1) {
+        if (s == STEN_OK)
+            s = c_dt == STEN_F32 ? launch_reduce<float>(parts, split, M, N, C, ldc, st)
+                                 : launch_reduce<bf16_t>(parts, split, M, N, C, ldc, st);
+        cudaFreeAsync(parts, st);
+    }
+    return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+sten_status sten_sparsify_grouped_nm(sten_nmg f, sten_dtype dt, const void* W, int64_t M, int64_t K,
+                                     int64_t ldw, void* values, uint8_t* idx, void* stream) {
+    sten_status s = check_format(f);
+    if (s) return s;
+    if (!dtype_ok(dt)) return STEN_ERR_INVALID_ARG;
+    if ((s = check_shape(f, M, K))) return s;
+    if (ldw < K) return STEN_ERR_SHAPE;
+    if (M * K > 0 && (!W || !values || !idx)) return STEN_ERR_INVALID_ARG;
+    const int64_t G = M / f.g, KB = K / f.m, Kp = KB * f.n;
+    if (G == 0 || KB == 0) return STEN_OK;
+    const bool aligned = aligned16(W) && (ldw * int64_t(dt_size(dt))) % 16 == 0;
+    cudaStream_t st = as_stream(stream);
+    bool ok = dt == STEN_F32 ? dispatch_sparsify<float>(f.m, W, ldw, G, KB, f, values, Kp, idx, aligned, st)
+                             : dispatch_sparsify<bf16_t>(f.m, W, ldw, G, KB, f, values, Kp, idx, aligned, st);
+    if (!ok) return STEN_ERR_UNSUPPORTED;
+    return last_cuda();
+}
+
+sten_status sten_densify(sten_nmg f, sten_dtype dt, const void* values, const uint8_t* idx, int64_t M,
+                         int64_t K, void* W_out, int64_t ldw, void* stream) {
+    sten_status s = check_format(f);
+    if (s) return s;
+    if (!dtype_ok(dt)) return STEN_ERR_INVALID_ARG;
+    if ((s = check_shape(f, M, K))) return s;
+    if (ldw < K) return STEN_ERR_SHAPE;
+    if (M * K > 0 && (!values || !idx || !W_out)) return STEN_ERR_INVALID_ARG;
+    const int64_t KB = K / f.m, Kp = KB * f.n;
+    if (M == 0 || KB == 0) return STEN_OK;
+    const bool aligned = aligned16(W_out) && (ldw * int64_t(dt_size(dt))) % 16 == 0;
+    cudaStream_t st = as_stream(stream);
+    bool ok = dt == STEN_F32 ? dispatch_densify<float>(f.m, values, idx, M, KB, f, Kp, W_out, ldw, aligned, st)
+                             : dispatch_densify<bf16_t>(f.m, values, idx, M, KB, f, Kp, W_out, ldw, aligned, st);
+    if (!ok) return STEN_ERR_UNSUPPORTED;
+    return last_cuda();
+}
+
+sten_status sten_spmm_plan_query(sten_nmg f, sten_dtype ab_dt, int64_t M, int64_t K, int64_t N,
+                                 sten_dtype c_dt, sten_spmm_plan* plan) {
+    sten_status s = check_format(f);
+    if (s) return s;
+    if (!plan || !dtype_ok(ab_dt) || !dtype_ok(c_dt)) return STEN_ERR_INVALID_ARG;
+    if ((s = check_shape(f, M, K))) return s;
+    if (N < 0) return STEN_ERR_SHAPE;
+    return plan_auto(f, ab_dt, M, K, N, c_dt, plan);
+}
+
+sten_status sten_spmm_grouped_nm_ex(sten_nmg f, sten_dtype ab_dt, const void* values, const uint8_t* idx,
+                                    int64_t M, int64_t K, const void* B, int64_t ldb, int64_t N, void* C,
+                                    int64_t ldc, sten_dtype c_dt, const sten_spmm_plan* plan, void* stream) {
+    return spmm_impl(f, ab_dt, values, idx, M, K, B, ldb, N, C, ldc, c_dt, plan, as_stream(stream));
+}
+
+sten_status sten_spmm_grouped_nm(sten_nmg f, sten_dtype ab_dt, const void* values, const uint8_t* idx,
+                                 int64_t M, int64_t K, const void* B, int64_t ldb, int64_t N, void* C,
+                                 int64_t ldc, sten_dtype c_dt, void* stream) {
+    return spmm_impl(f, ab_dt, values, idx, M, K, B, ldb, N, C, ldc, c_dt, nullptr, as_stream(stream));
+}
+
+// ---- end-to-end host entry point --------------------------------------------------------------
+static inline int64_t round16(int64_t b) { return (b + 15) & ~int64_t(15); }
+
+int64_t sten_sparse_linear_host_workspace_size(sten_nmg f, sten_dtype ab_dt, int64_t M, int64_t K,
+                                               int64_t N, sten_dtype c_dt) {
+    if (check_format(f) || check_shape(f, M, K) || N < 0 || !dtype_ok(ab_dt) || !dtype_ok(c_dt)) return -1;
+    const int64_t s = int64_t(dt_size(ab_dt));
+    const int64_t Kp = K / f.m * f.n;
+    const int64_t ldb = (N * s + 15) / 16 * 16 / s;
+    const int64_t ldc = (N * int64_t(dt_size(c_dt)) + 15) / 16 * 16 / int64_t(dt_size(c_dt));
+    return round16(M * K * s) + round16(M * Kp * s) + round16(M / f.g * (K / f.m) * f.n) +
+           round16(K * ldb * s) + round16(M * ldc * int64_t(dt_size(c_dt)));
+}
+
+sten_status sten_sparse_linear_host(sten_nmg f, sten_dtype ab_dt, const void* W_host, int64_t M, int64_t K,
+                                    int64_t ldw, const void* B_host, int64_t ldb, int64_t N, void* C_host,
+                                    int64_t ldc, sten_dtype c_dt, void* workspace, int64_t workspace_bytes,
+                                    void* stream) {
+    sten_status s = check_format(f);
+    if (s) return s;
+    if (!dtype_ok(ab_dt) || !dtype_ok(c_dt)) return STEN_ERR_INVALID_ARG;
+    if (!W_host || !B_host || !C_host || !workspace) return STEN_ERR_INVALID_ARG;
+    if ((s = check_shape(f, M, K))) return s;
+    if (N < 0 || ldw < K || ldb < N || ldc < N) return STEN_ERR_SHAPE;
+    const int64_t need = sten_sparse_linear_host_workspace_size(f, ab_dt, M, K, N, c_dt);
+    if (need < 0 || workspace_bytes < need || !aligned16(workspace)) return STEN_ERR_INVALID_ARG;
+    const int64_t sab = int64_t(dt_size(ab_dt)), sc = int64_t(dt_size(c_dt));
+    const int64_t Kp = K / f.m * f.n;
+    const int64_t dldb = (N * sab + 15) / 16 * 16 / sab;
+    const int64_t dldc = (N * sc + 15) / 16 * 16 / sc;
+    char* p = static_cast<char*>(workspace);
+    void* dW = p;             p += round16(M * K * sab);
+    void* dV = p;             p += round16(M * Kp * sab);
+    uint8_t* dI = reinterpret_cast<uint8_t*>(p); p += round16(M / f.g * (K / f.m) * f.n);
+    void* dB = p;             p += round16(K * dldb * sab);
+    void* dC = p;
+    cudaStream_t st = as_stream(stream);
+    if (M * K > 0 &&
+        cudaMemcpy2DAsync(dW, size_t(K * sab), W_host, size_t(ldw * sab), size_t(K * sab), size_t(M),
+                          cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return STEN_ERR_CUDA;
+    if (K * N > 0 &&
+        cudaMemcpy2DAsync(dB, size_t(dldb * sab), B_host, size_t(ldb * sab), size_t(N * sab), size_t(K),
+                          cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return STEN_ERR_CUDA;
+    if ((s = sten_sparsify_grouped_nm(f, ab_dt, dW, M, K, K, dV, dI, stream))) return s;
+    if ((s = spmm_impl(f, ab_dt, dV, dI, M, K, dB, dldb, N, dC, dldc, c_dt, nullptr, st))) return s;
+    if (M * N > 0 &&
+        cudaMemcpy2DAsync(C_host, size_t(ldc * sc), dC, size_t(dldc * sc), size_t(N * sc), size_t(M),
+                          cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        return STEN_ERR_CUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return STEN_ERR_CUDA;
+    return STEN_OK;
+}
+
+const char* sten_status_string(sten_status s) {
+    switch (s) {
+        case STEN_OK: return "STEN_OK";
+        case STEN_ERR_INVALID_ARG: return "STEN_ERR_INVALID_ARG";
+        case STEN_ERR_SHAPE: return "STEN_ERR_SHAPE";
+        case STEN_ERR_UNSUPPORTED: return "STEN_ERR_UNSUPPORTED";
+        case STEN_ERR_CUDA: return "STEN_ERR_CUDA";
+    }
+    return "STEN_ERR_UNKNOWN";
+}
+
+const char* sten_algo_name(int32_t algo) {
+    switch (algo) {
+        case STEN_ALGO_AUTO: return "auto";
+        case STEN_ALGO_SIMT: return "simt";
+        case STEN_ALGO_MMA_SYNC: return "mma_sync";
+        case STEN_ALGO_TCGEN05: return "tcgen05";
+    }
+    return "unknown";
+}
+
+int32_t sten_spmm_launch_count(const sten_spmm_plan* plan) {
+    if (!plan) return 1;
+    return plan->split_k > 1 ? 2 : 1;
+}
+
+int32_t sten_version(void) { return 1; }
+
+}  // extern "C"

@@ -1,0 +1,216 @@
+"""Thin ctypes binding of the C ABI in include/sten.h (argument marshalling only).
+
+Every function forwards torch CUDA tensors' device pointers and the current
+CUDA stream to ``libsten.so``; all computation happens in the library's
+sm_100a kernels.  There is no CPU fallback: if the library or a CUDA device is
+missing, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from . import build as _build
+
+F32, BF16 = 0, 1
+ALGO_AUTO, ALGO_SIMT, ALGO_MMA_SYNC, ALGO_TCGEN05 = 0, 1, 2, 3
+_STATUS = {0: "STEN_OK", 1: "STEN_ERR_INVALID_ARG", 2: "STEN_ERR_SHAPE",
+           3: "STEN_ERR_UNSUPPORTED", 4: "STEN_ERR_CUDA"}
+
+
+class StenError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__("%s failed: %s" % (what, _STATUS.get(status, status)))
+        self.status = status
+
+
+class sten_nmg(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("m", ctypes.c_int32), ("g", ctypes.c_int32)]
+
+
+class sten_spmm_plan(ctypes.Structure):
+    _fields_ = [("algo", ctypes.c_int32), ("split_k", ctypes.c_int32), ("tile", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
+
+    def as_dict(self):
+        return {"algo": self.algo, "split_k": self.split_k, "tile": self.tile}
+
+
+_lib = None
+_i64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+
+# exported symbols and their ctypes signatures (kept in sync with include/sten.h)
+SIGNATURES = {
+    "sten_sparsify_grouped_nm": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "sten_densify": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
+    "sten_spmm_grouped_nm": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64, _i64,
+                                            _vp, _i64, ctypes.c_int, _vp]),
+    "sten_spmm_plan_query": (ctypes.c_int, [sten_nmg, ctypes.c_int, _i64, _i64, _i64, ctypes.c_int,
+                                            ctypes.POINTER(sten_spmm_plan)]),
+    "sten_spmm_grouped_nm_ex": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64, _i64,
+                                               _vp, _i64, ctypes.c_int, ctypes.POINTER(sten_spmm_plan), _vp]),
+    "sten_sparse_linear_host_workspace_size": (ctypes.c_int64, [sten_nmg, ctypes.c_int, _i64, _i64, _i64,
+                                                                ctypes.c_int]),
+    "sten_sparse_linear_host": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _i64, _i64,
+                                               _vp, _i64, ctypes.c_int, _vp, _i64, _vp]),
+    "sten_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "sten_algo_name": (ctypes.c_char_p, [ctypes.c_int32]),
+    "sten_spmm_launch_count": (ctypes.c_int32, [ctypes.POINTER(sten_spmm_plan)]),
+    "sten_version": (ctypes.c_int32, []),
+}
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True):
+    """Load libsten.so (building it in-tree first if it is missing or stale)."""
+    global _lib
+    if _lib is None:
+        if build_if_missing and _build.needs_build():
+            _build.build()
+        if not os.path.exists(_build.LIB):
+            raise RuntimeError("libsten.so is missing (run paper_2304_07613_b200/build.py); "
+                               "there is no CPU fallback")
+        lib = ctypes.CDLL(_build.LIB)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return F32
+    if t.dtype == torch.bfloat16:
+        return BF16
+    raise TypeError("sten supports float32 and bfloat16 tensors, got %s" % t.dtype)
+
+
+def _torch_dtype(code: int):
+    return torch.float32 if code == F32 else torch.bfloat16
+
+
+def _cuda(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError("%s must be a CUDA tensor (no CPU fallback)" % name)
+    if t.dim() != 2 and name not in ("idx",):
+        raise ValueError("%s must be 2-D" % name)
+
+
+def _ld(t: torch.Tensor) -> int:
+    if t.stride(-1) != 1:
+        raise ValueError("innermost dimension must be contiguous")
+    return t.stride(0) if t.dim() == 2 else t.shape[-1]
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise StenError(status, what)
+
+
+def sparsify_grouped_nm(W: torch.Tensor, n: int, m: int, g: int, values: torch.Tensor | None = None,
+                        idx: torch.Tensor | None = None, stream=None):
+    """a1-a3: dense W [M][K] -> (values [M][K/m*n], idx [M/g][K/m][n] uint8)."""
+    _cuda(W, "W")
+    M, K = W.shape
+    if values is None:
+        values = torch.empty((M, K // m * n if m else 0), dtype=W.dtype, device=W.device)
+    if idx is None:
+        idx = torch.empty((M // g if g else 0, K // m if m else 0, n), dtype=torch.uint8, device=W.device)
+    _check(load().sten_sparsify_grouped_nm(sten_nmg(n, m, g), _dt(W), W.data_ptr(), M, K, _ld(W),
+                                           values.data_ptr(), idx.data_ptr(), _stream(stream)),
+           "sten_sparsify_grouped_nm")
+    return values, idx
+
+
+def densify(values: torch.Tensor, idx: torch.Tensor, n: int, m: int, g: int, K: int,
+            out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """a4: grouped n:m -> dense [M][K] (zeros at pruned positions)."""
+    _cuda(values, "values")
+    M = values.shape[0]
+    if out is None:
+        out = torch.empty((M, K), dtype=values.dtype, device=values.device)
+    _check(load().sten_densify(sten_nmg(n, m, g), _dt(values), values.data_ptr(), idx.data_ptr(), M, K,
+                               out.data_ptr(), _ld(out), _stream(stream)), "sten_densify")
+    return out
+
+
+def spmm_plan(n: int, m: int, g: int, M: int, K: int, N: int, ab_dtype=torch.float32,
+              c_dtype=None) -> sten_spmm_plan:
+    plan = sten_spmm_plan()
+    ab = F32 if ab_dtype == torch.float32 else BF16
+    c = ab if c_dtype is None else (F32 if c_dtype == torch.float32 else BF16)
+    _check(load().sten_spmm_plan_query(sten_nmg(n, m, g), ab, M, K, N, c, ctypes.byref(plan)),
+           "sten_spmm_plan_query")
+    return plan
+
+
+def make_plan(algo: int = ALGO_AUTO, split_k: int = 0, tile: int = 0) -> sten_spmm_plan:
+    p = sten_spmm_plan()
+    p.algo, p.split_k, p.tile = algo, split_k, tile
+    return p
+
+
+def spmm_grouped_nm(values: torch.Tensor, idx: torch.Tensor, B: torch.Tensor, n: int, m: int, g: int,
+                    out: torch.Tensor | None = None, out_dtype=None, plan: sten_spmm_plan | None = None,
+                    stream=None) -> torch.Tensor:
+    """a5-a7: C [M][N] = densify(values, idx) @ B  (B [K][N])."""
+    _cuda(values, "values")
+    _cuda(B, "B")
+    M = values.shape[0]
+    K, N = B.shape
+    if values.dtype != B.dtype:
+        raise TypeError("values and B must share a dtype")
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype or B.dtype, device=B.device)
+    lib = load()
+    args = (sten_nmg(n, m, g), _dt(B), values.data_ptr(), idx.data_ptr(), M, K, B.data_ptr(), _ld(B), N,
+            out.data_ptr(), _ld(out), _dt(out))
+    if plan is None:
+        _check(lib.sten_spmm_grouped_nm(*args, _stream(stream)), "sten_spmm_grouped_nm")
+    else:
+        _check(lib.sten_spmm_grouped_nm_ex(*args, ctypes.byref(plan), _stream(stream)), "sten_spmm_grouped_nm_ex")
+    return out
+
+
+def sparse_linear_host(W_host: torch.Tensor, B_host: torch.Tensor, n: int, m: int, g: int,
+                       C_host: torch.Tensor, workspace: torch.Tensor, stream=None) -> torch.Tensor:
+    """End-to-end: host W, host B -> host C through sten_sparse_linear_host (blocking)."""
+    M, K = W_host.shape
+    N = B_host.shape[1]
+    _check(load().sten_sparse_linear_host(sten_nmg(n, m, g), _dt(W_host), W_host.data_ptr(), M, K, _ld(W_host),
+                                          B_host.data_ptr(), _ld(B_host), N, C_host.data_ptr(), _ld(C_host),
+                                          _dt(C_host), workspace.data_ptr(), workspace.numel(), _stream(stream)),
+           "sten_sparse_linear_host")
+    return C_host
+
+
+def sparse_linear_host_workspace_size(n: int, m: int, g: int, M: int, K: int, N: int,
+                                      ab_dtype=torch.float32, c_dtype=torch.float32) -> int:
+    return int(load().sten_sparse_linear_host_workspace_size(
+        sten_nmg(n, m, g), F32 if ab_dtype == torch.float32 else BF16, M, K, N,
+        F32 if c_dtype == torch.float32 else BF16))
+
+
+def launch_count(plan: sten_spmm_plan) -> int:
+    return int(load().sten_spmm_launch_count(ctypes.byref(plan)))
+
+
+def algo_name(algo: int) -> str:
+    return load().sten_algo_name(algo).decode()
+
+
+def status_string(s: int) -> str:
+    return load().sten_status_string(s).decode()

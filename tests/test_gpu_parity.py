@@ -1,0 +1,270 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle (-m gpu).
+
+Bars (BASELINE.json north_star):
+  * idx and values: bit-exact;  densify: bit-exact;
+  * C (fp32 in, fp32 out): max_{r,c} |C - C_ref| / Bound[r,c] <= 1e-5,
+    Bound = sum |v| |b| (fp64, from the oracle);
+  * C (bf16 in):          same metric <= 2e-2;
+  * integer-valued inputs (P7) and B = I (P8): bit-exact on every path;
+  * column-sharded == unsharded (P11): bit-exact with the same plan.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthetic
+from paper_2304_07613_b200 import sten
+
+pytestmark = pytest.mark.gpu
+
+NM_SET = [(1, 2), (2, 4), (1, 4), (2, 8), (1, 8), (1, 10), (1, 12), (3, 6), (4, 16)]
+TOL = {"f32": 1e-5, "bf16": 2e-2}
+
+
+def dev(x: np.ndarray, dtype: str, ld_multiple: int = 8) -> torch.Tensor:
+    """Device copy of a 2-D host array whose leading dimension is padded to a
+    multiple of `ld_multiple` elements (the ABI wants 16-byte aligned rows);
+    returns the [rows][cols] view."""
+    x = np.ascontiguousarray(x)
+    rows, cols = x.shape
+    ld = -(-cols // ld_multiple) * ld_multiple if cols else ld_multiple
+    if dtype == "bf16":
+        t = torch.zeros((rows, ld), dtype=torch.bfloat16)
+        t[:, :cols] = torch.from_numpy(x.view(np.int16)).view(torch.bfloat16)
+    else:
+        t = torch.zeros((rows, ld), dtype=torch.float32)
+        t[:, :cols] = torch.from_numpy(x)
+    return t.cuda()[:, :cols]
+
+
+def host(t: torch.Tensor) -> np.ndarray:
+    t = t.cpu()
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).numpy().view(np.uint16)
+    return t.numpy()
+
+
+def rel_err(C: torch.Tensor, C_ref: np.ndarray, Bound: np.ndarray) -> float:
+    c = C.float().cpu().numpy().astype(np.float64)
+    return float(np.max(np.abs(c - C_ref) / np.maximum(Bound, 1e-30))) if c.size else 0.0
+
+
+def gpu_sparsify(W, n, m, g, dtype):
+    v, i = sten.sparsify_grouped_nm(dev(W, dtype), n, m, g)
+    torch.cuda.synchronize()
+    return v, i
+
+
+# ----------------------------------------------------------------------------------------
+# K1 sparsify / K2 densify: bit-exact
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n,m", NM_SET)
+@pytest.mark.parametrize("g", [1, 3, 4, 16])
+def test_sparsify_densify_bit_exact(dtype, n, m, g):
+    M, K = 8 * g, 37 * m            # ragged: 37 blocks spans >1 warp, odd counts
+    W = synthetic.weights(M, K, seed=n * 100 + m * 10 + g, dtype=dtype)
+    if dtype == "f32":
+        W[:g, :m] = 0.25                       # a tied block
+    v_ref, i_ref = oracle.sparsify(W, n, m, g)
+    v, i = gpu_sparsify(W, n, m, g, dtype)
+    assert np.array_equal(host(i), i_ref)
+    assert np.array_equal(host(v).view(np.uint8), v_ref.view(np.uint8))
+    Wd = sten.densify(v, i, n, m, g, K)
+    assert np.array_equal(host(Wd).view(np.uint8), oracle.densify(v_ref, i_ref, n, m, g, K).view(np.uint8))
+
+
+def test_sparsify_unaligned_ld_and_integer_ties():
+    n, m, g = 2, 4, 4
+    W = synthetic.integer_matrix(16, 44, seed=3, lo=-2, hi=2)
+    Wt = torch.from_numpy(np.pad(W, ((0, 0), (0, 1)))).cuda()[:, :44]   # ldw = 45: scalar path
+    v, i = sten.sparsify_grouped_nm(Wt, n, m, g)
+    v_ref, i_ref = oracle.sparsify(W, n, m, g)
+    assert np.array_equal(host(i), i_ref) and np.array_equal(host(v), v_ref)
+    assert np.array_equal(host(i), oracle.brute_select(W, n, m, g))
+
+
+def test_sparsify_large_group_and_fp32_near_ties():
+    n, m, g = 1, 2, 3
+    e = np.float32(2.0 ** -24)
+    W = np.array([[1.0, 1.0 + 2.0 ** -23], [e, 0.0], [e, 0.0]], np.float32)
+    _, i = gpu_sparsify(W, n, m, g, "f32")
+    assert host(i).tolist() == [[[1]]]                  # fp32 score rule (reading R4)
+    W = synthetic.weights(128, 64, seed=1)
+    for g in (32, 64, 128):
+        v_ref, i_ref = oracle.sparsify(W, 2, 4, g)
+        v, i = gpu_sparsify(W, 2, 4, g, "f32")
+        assert np.array_equal(host(i), i_ref) and np.array_equal(host(v), v_ref)
+
+
+def test_p0_worked_example_on_gpu(golden_dir):
+    import json, os
+    ex = json.load(open(os.path.join(golden_dir, "p0_worked_example.json")))
+    W = np.array(ex["W"], np.float32)
+    v, i = gpu_sparsify(W, ex["n"], ex["m"], ex["g"], "f32")
+    assert host(i).tolist() == ex["idx"] and host(v).tolist() == ex["values"]
+    B = torch.tensor([[k + 1, 1] + [0, 0] for k in range(8)], dtype=torch.float32).cuda()  # ldb = 4
+    C = sten.spmm_grouped_nm(v, i, B[:, :2], ex["n"], ex["m"], ex["g"])
+    assert C.cpu().tolist() == ex["C"]
+
+
+# ----------------------------------------------------------------------------------------
+# SpMM parity on every algorithm / tile / split
+# ----------------------------------------------------------------------------------------
+SIMT_TILES = [1, 2, 3, 4]
+
+
+def _spmm_case(M, K, N, n, m, g, dtype, plan=None, out_dtype=None, seed=0):
+    W = synthetic.weights(M, K, seed=seed + 1, dtype=dtype)
+    B = synthetic.activations(K, N, seed=seed + 2, dtype=dtype)
+    v_ref, i_ref = oracle.sparsify(W, n, m, g)
+    C_ref, Bound = oracle.spmm(v_ref, i_ref, B, n, m, g, nthreads=oracle.max_threads())
+    v, i = gpu_sparsify(W, n, m, g, dtype)
+    C = sten.spmm_grouped_nm(v, i, dev(B, dtype), n, m, g, plan=plan, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    return C, C_ref, Bound
+
+
+@pytest.mark.parametrize("tile", SIMT_TILES)
+@pytest.mark.parametrize("g", [1, 2, 4, 8])
+@pytest.mark.parametrize("split", [1, 3])
+def test_spmm_simt_f32(tile, g, split):
+    rg = 8 if g % 8 == 0 else 4 if g % 4 == 0 else 2 if g % 2 == 0 else 1
+    if rg * {1: 8, 2: 8, 3: 8, 4: 4}[tile] * {1: 1, 2: 2, 3: 4, 4: 8}[tile] > 128:
+        pytest.skip("tile not compiled for this g")
+    plan = sten.make_plan(sten.ALGO_SIMT, split_k=split, tile=tile)
+    # M not a multiple of the CTA rows, N ragged (not a multiple of 4*32), several K slabs
+    C, C_ref, Bound = _spmm_case(M=40 * g if g < 8 else 24 * g, K=200, N=301, n=2, m=4, g=g, dtype="f32",
+                                 plan=plan, seed=tile * 10 + g)
+    assert rel_err(C, C_ref, Bound) <= TOL["f32"]
+
+
+@pytest.mark.parametrize("n,m", NM_SET)
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_spmm_auto_all_formats(n, m, dtype):
+    g = 4
+    C, C_ref, Bound = _spmm_case(M=96, K=24 * m, N=160, n=n, m=m, g=g, dtype=dtype, seed=n + m,
+                                 out_dtype=torch.float32)
+    assert rel_err(C, C_ref, Bound) <= 1e-5     # fp32 output: only fp32 accumulation error
+
+
+@pytest.mark.parametrize("g", [8, 16, 64])
+@pytest.mark.parametrize("n,m", [(2, 4), (1, 4), (1, 10), (3, 6)])
+@pytest.mark.parametrize("split", [1, 2])
+def test_spmm_mma_bf16(g, n, m, split):
+    tile = 2 if g % 16 == 0 else 1
+    plan = sten.make_plan(sten.ALGO_MMA_SYNC, split_k=split, tile=tile)
+    C, C_ref, Bound = _spmm_case(M=max(2 * g, 320), K=40 * m, N=200, n=n, m=m, g=g, dtype="bf16", plan=plan,
+                                 out_dtype=torch.float32, seed=g + n + m)
+    assert rel_err(C, C_ref, Bound) <= 1e-5     # fp32 output: only fp32 accumulation error
+    plan1 = sten.make_plan(sten.ALGO_MMA_SYNC, split_k=split, tile=1)
+    C1, _, _ = _spmm_case(M=max(2 * g, 320), K=40 * m, N=200, n=n, m=m, g=g, dtype="bf16", plan=plan1,
+                          out_dtype=torch.bfloat16, seed=g + n + m)
+    assert rel_err(C1, C_ref, Bound) <= TOL["bf16"]
+
+
+@pytest.mark.parametrize("algo,dtype,g", [(sten.ALGO_SIMT, "f32", 4), (sten.ALGO_SIMT, "bf16", 4),
+                                          (sten.ALGO_MMA_SYNC, "bf16", 16)])
+def test_p7_integer_exact(algo, dtype, g):
+    n, m = 2, 4
+    M, K, N = 4 * g * 8, 64, 136
+    W = synthetic.integer_matrix(M, K, seed=1, dtype=dtype)
+    B = synthetic.integer_matrix(K, N, seed=2, dtype=dtype)
+    v_ref, i_ref = oracle.sparsify(W, n, m, g)
+    C_ref, _ = oracle.spmm(v_ref, i_ref, B, n, m, g)
+    v, i = gpu_sparsify(W, n, m, g, dtype)
+    C = sten.spmm_grouped_nm(v, i, dev(B, dtype), n, m, g, plan=sten.make_plan(algo, split_k=2),
+                             out_dtype=torch.float32)
+    assert np.array_equal(C.cpu().numpy().astype(np.float64), C_ref)
+
+
+@pytest.mark.parametrize("dtype,g", [("f32", 4), ("bf16", 8)])
+def test_p8_identity_gives_densify(dtype, g):
+    n, m, K = 1, 4, 64
+    W = synthetic.weights(2 * g, K, seed=4, dtype=dtype)
+    v, i = gpu_sparsify(W, n, m, g, dtype)
+    I = torch.eye(K, dtype=torch.float32 if dtype == "f32" else torch.bfloat16).cuda()
+    C = sten.spmm_grouped_nm(v, i, I, n, m, g)
+    D = sten.densify(v, i, n, m, g, K)
+    assert torch.equal(C, D)
+
+
+def test_p9_spec_example():
+    v, i = gpu_sparsify(np.array([[2, 0], [0, 3]], np.float32), 1, 2, 1, "f32")
+    B = torch.ones((2, 4), dtype=torch.float32).cuda()
+    assert sten.spmm_grouped_nm(v, i, B[:, :2], 1, 2, 1).cpu().tolist() == [[2, 2], [3, 3]]
+
+
+# ----------------------------------------------------------------------------------------
+# P11: column shards == unsharded (same plan), edge cases, errors
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype,g", [("f32", 4), ("bf16", 16)])
+def test_p11_column_shards_bit_exact(dtype, g):
+    n, m, M, K, N, P = 1, 4, 256, 512, 1024, 4
+    W = synthetic.weights(M, K, seed=8, dtype=dtype)
+    B = dev(synthetic.activations(K, N, seed=8, dtype=dtype), dtype)
+    v, i = gpu_sparsify(W, n, m, g, dtype)
+    plan = sten.spmm_plan(n, m, g, M, K, N, ab_dtype=B.dtype, c_dtype=torch.float32)
+    full = sten.spmm_grouped_nm(v, i, B, n, m, g, plan=plan, out_dtype=torch.float32)
+    for p in range(P):
+        cols = slice(p * N // P, (p + 1) * N // P)
+        shard = sten.spmm_grouped_nm(v, i, B[:, cols], n, m, g, plan=plan, out_dtype=torch.float32)
+        assert torch.equal(shard, full[:, cols])
+
+
+def test_empty_and_k_zero():
+    v = torch.empty((8, 0), dtype=torch.float32, device="cuda")
+    i = torch.empty((2, 0, 2), dtype=torch.uint8, device="cuda")
+    B = torch.empty((0, 16), dtype=torch.float32, device="cuda")
+    C = torch.full((8, 16), 7.0, device="cuda")
+    sten.spmm_grouped_nm(v, i, B, 2, 4, 4, out=C)
+    assert torch.count_nonzero(C).item() == 0
+    B2 = torch.empty((16, 0), dtype=torch.float32, device="cuda")
+    v2, i2 = sten.sparsify_grouped_nm(torch.randn(8, 16, device="cuda"), 2, 4, 4)
+    assert sten.spmm_grouped_nm(v2, i2, B2, 2, 4, 4).shape == (8, 0)
+
+
+def test_error_leaves_outputs_untouched():
+    W = torch.randn(12, 16, device="cuda")
+    v = torch.full((12, 8), 5.0, device="cuda")
+    i = torch.full((3, 4, 2), 9, dtype=torch.uint8, device="cuda")
+    with pytest.raises(sten.StenError):
+        sten.sparsify_grouped_nm(W, 2, 4, 5, values=v, idx=i)      # 12 % 5 != 0
+    assert torch.all(v == 5.0) and torch.all(i == 9)
+
+
+def test_host_e2e_entry_point():
+    n, m, g, M, K, N = 2, 4, 4, 64, 128, 96
+    W = synthetic.weights(M, K, seed=5)
+    B = synthetic.activations(K, N, seed=5)
+    Wh = torch.from_numpy(W).pin_memory()
+    Bh = torch.from_numpy(B).pin_memory()
+    Ch = torch.empty((M, N), dtype=torch.float32).pin_memory()
+    ws = torch.empty(sten.sparse_linear_host_workspace_size(n, m, g, M, K, N), dtype=torch.uint8, device="cuda")
+    sten.sparse_linear_host(Wh, Bh, n, m, g, Ch, ws)
+    v_ref, i_ref = oracle.sparsify(W, n, m, g)
+    C_ref, Bound = oracle.spmm(v_ref, i_ref, B, n, m, g)
+    assert rel_err(Ch, C_ref, Bound) <= 1e-5
+
+
+# ----------------------------------------------------------------------------------------
+# BASELINE.json sizes, in the launch configuration bench.py uses: sampled outputs
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_baseline_configs_sampled(cfg):
+    rng = np.random.default_rng(cfg)
+    cases = synthetic.config_cases(cfg, g=4 if cfg == 1 else 16)
+    for case in cases[:: 3 if cfg == 1 else 1]:
+        W = synthetic.weights(case.M, case.K, seed=1234 + cfg, dtype=case.dtype, k_pad=case.k_pad)
+        B = synthetic.activations(case.K, case.N, seed=1234 + cfg, dtype=case.dtype, k_pad=case.k_pad)
+        v_ref, i_ref = oracle.sparsify(W, case.n, case.m, case.g)
+        v, i = gpu_sparsify(W, case.n, case.m, case.g, case.dtype)
+        assert np.array_equal(host(i), i_ref)
+        C = sten.spmm_grouped_nm(v, i, dev(B, case.dtype), case.n, case.m, case.g, out_dtype=torch.float32)
+        cols = np.sort(rng.choice(case.N, size=24, replace=False))
+        Cs = C.cpu().numpy()[:, cols].astype(np.float64)
+        C_ref, Bound = oracle.spmm(v_ref, i_ref, np.ascontiguousarray(B[:, cols]), case.n, case.m, case.g,
+                                   nthreads=oracle.max_threads())
+        assert float(np.max(np.abs(Cs - C_ref) / np.maximum(Bound, 1e-30))) <= TOL[case.dtype] * (
+            1 if case.dtype == "f32" else 0.05), case.label()
