@@ -1,0 +1,578 @@
+#!/usr/bin/env python
+"""Benchmark of the grouped n:m hot path (sparsify + SpMM) -- the driver contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sten|reference]
+                    [--config 1] [--dtype f32|bf16] [--g 4]
+
+A STEP is one pass of the whole hot path over one batch of synthetic input:
+for every case of the BASELINE.json config, a1-a3 (sparsify the dense weight
+into grouped n:m) and a5-a7 (the grouped-n:m x dense SpMM).  Default workload
+= BASELINE.json configs[1]: BERT-base linears 768x768, 768x3072, 3072x768 at
+2:4 / 1:4 / 1:10 (K zero-padded to a multiple of 10), g = 4, batch 8 x seq 128
+= 1024 tokens, fp32 (the paper's CPU kernel precision).
+
+metric = effective (dense-equivalent) GFLOP/s = sum_cases 2*M*K*N / step time
+(SPEC.md:311 convention).  Under torchrun every rank runs its own batch (weak
+scaling: tokens are independent columns, no collective on this path); value
+= all ranks' flops / max-over-ranks time.  --config 4 runs the column-sharded
+8192^2 x 65536 product with the NCCL all-gather of C instead (strong scaling).
+
+L2 hygiene: the timed loop cycles through R device copies of the inputs whose
+total size exceeds 3x the L2 (config["l2"]).  Each input set's step is one CUDA
+graph; the SpMM launches inside it are bracketed by external event-record
+nodes so the dominant kernel is timed live on its own stream.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synthetic  # noqa: E402
+
+METRIC = "grouped n:m SpMM effective GFLOP/s + % roofline at 1/2/4/8 B200 (BERT shapes)"
+UNIT = "GFLOP/s"
+CONFIG_NAMES = {
+    0: "C1 tiny grouped 2:4 SpMM 64x64, g=4, 32 tokens",
+    1: "C2 BERT-base linears {768x768,768x3072,3072x768} x {2:4,1:4,1:10} x 1024 tokens",
+    2: "C3 BERT-large linears {1024x4096,4096x1024} x {1:4,2:8} x 16384 tokens",
+    3: "C4 BERT-base encoder-layer linears (QKV,O,FFN1,FFN2) 2:4 x 32768 tokens",
+    4: "C5 8192x8192 1:8 x 65536 tokens, column-sharded + NCCL all-gather",
+}
+FP32_LANES_PER_SM = 128        # B200 CUDA-core FP32 lanes per SM (guide unit counts)
+NUM_SMS = 148
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["sten", "reference"], default="sten")
+    p.add_argument("--config", type=int, default=1)
+    p.add_argument("--dtype", choices=["f32", "bf16"], default=None)
+    p.add_argument("--g", type=int, default=None)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu legs)")
+    p.add_argument("--out", default=None, help="also append the JSON line to this file")
+    return p.parse_args()
+
+
+def default_dtype_g(cfg: int):
+    return {0: ("f32", 4), 1: ("f32", 4), 2: ("bf16", 16), 3: ("f32", 4), 4: ("f32", 4)}[cfg]
+
+
+def cases_for(cfg, g, dtype):
+    cases = synthetic.config_cases(cfg, g=g, dtype=dtype)
+    if cfg == 2:
+        cases = [synthetic.Case(c.M, c.K, c.N, c.n, c.m, g, dtype) for c in cases]
+    return cases
+
+
+def eff_flops(c) -> float:          # dense-equivalent, true (unpadded) K
+    return 2.0 * c.M * c.K * c.N
+
+
+def nz_flops(c) -> float:           # algorithmic MACs actually required (kept K', incl. K padding)
+    return 2.0 * c.M * c.kept * c.N
+
+
+def esize(dtype):
+    return 4 if dtype == "f32" else 2
+
+
+def spmm_bytes(c, out_size=None) -> float:
+    s = esize(c.dtype)
+    so = s if out_size is None else out_size
+    return c.M * c.kept * s + (c.M // c.g) * (c.Kp // c.m) * c.n + c.Kp * c.N * s + c.M * c.N * so
+
+
+def cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    rows.append((float(parts[1]), float(parts[2]), float(parts[3]), parts[5:9]))
+                except ValueError:
+                    continue
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        loaded = [r for r in rows if r[2] > 200.0] or rows
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in loaded:
+            for nm, v in zip(names, r[3]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": sorted(reasons), "samples": len(rows), "samples_under_load": len(loaded),
+                "power_w_max": max(r[2] for r in rows)}
+
+
+# ------------------------------------------------------------------------------------------------
+# the timed GPU step
+# ------------------------------------------------------------------------------------------------
+class ExtEvents:
+    """Timing events recorded as external event nodes (valid inside CUDA graph capture)."""
+
+    def __init__(self):
+        self.rt = ctypes.CDLL("libcudart.so.12")
+        self.rt.cudaEventRecordWithFlags.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint]
+
+    def record(self, ev, stream):
+        rc = self.rt.cudaEventRecordWithFlags(ctypes.c_void_p(ev._as_parameter_.value
+                                                              if hasattr(ev._as_parameter_, "value")
+                                                              else ev._as_parameter_),
+                                              ctypes.c_void_p(stream.cuda_stream), 1)
+        if rc != 0:
+            raise RuntimeError("cudaEventRecordWithFlags failed: %d" % rc)
+
+
+def make_sets(cases, R, device, dtype):
+    import torch
+    from paper_2304_07613_b200 import sten
+    sets = []
+    host = []
+    for ci, c in enumerate(cases):
+        W = synthetic.weights(c.M, c.K, seed=1234 + ci, dtype=c.dtype, k_pad=c.k_pad)
+        B = synthetic.activations(c.K, c.N, seed=1234 + ci, dtype=c.dtype, k_pad=c.k_pad)
+        host.append((W, B))
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    for _ in range(R):
+        data = []
+        for c, (W, B) in zip(cases, host):
+            Wt = torch.from_numpy(W.view(np.int16) if dtype == "bf16" else W)
+            Bt = torch.from_numpy(B.view(np.int16) if dtype == "bf16" else B)
+            if dtype == "bf16":
+                Wt, Bt = Wt.view(torch.bfloat16), Bt.view(torch.bfloat16)
+            Wd, Bd = Wt.to(device), Bt.to(device)
+            vals = torch.empty((c.M, c.kept), dtype=tdt, device=device)
+            idx = torch.empty((c.M // c.g, c.Kp // c.m, c.n), dtype=torch.uint8, device=device)
+            C = torch.empty((c.M, c.N), dtype=tdt, device=device)
+            plan = sten.spmm_plan(c.n, c.m, c.g, c.M, c.Kp, c.N, ab_dtype=tdt, c_dtype=tdt)
+            data.append(dict(W=Wd, B=Bd, values=vals, idx=idx, C=C, plan=plan))
+        sets.append(data)
+    return sets, host
+
+
+def run_step(cases, data, ev_pairs=None, ext=None, stream=None):
+    from paper_2304_07613_b200 import sten
+    for k, (c, d) in enumerate(zip(cases, data)):
+        sten.sparsify_grouped_nm(d["W"], c.n, c.m, c.g, values=d["values"], idx=d["idx"])
+        if ev_pairs is not None:
+            ext.record(ev_pairs[k][0], stream)
+        sten.spmm_grouped_nm(d["values"], d["idx"], d["B"], c.n, c.m, c.g, out=d["C"], plan=d["plan"])
+        if ev_pairs is not None:
+            ext.record(ev_pairs[k][1], stream)
+
+
+def bench_sten(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2304_07613_b200 import sten
+
+    cfg = args.config
+    dtype, g = default_dtype_g(cfg)
+    dtype = args.dtype or dtype
+    g = args.g or g
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    sten.load()
+    cases = cases_for(cfg, g, dtype)
+    props = torch.cuda.get_device_properties(device)
+    l2 = getattr(props, "L2_cache_size", 126 * 2 ** 20)
+    set_bytes = sum(c.M * c.Kp * esize(dtype) + spmm_bytes(c) for c in cases)
+    R = int(min(8, max(2, math.ceil(3 * l2 / set_bytes))))
+    free, _ = torch.cuda.mem_get_info(device)
+    R = max(1, min(R, int(0.6 * free // max(1, set_bytes))))
+    sets, host = make_sets(cases, R, device, dtype)
+    stream = torch.cuda.Stream(device)
+    ext = ExtEvents()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in cases]
+          for _ in range(R)]
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(R)]
+
+    # warm-up (also JIT-free: the library is precompiled) then capture one graph per set;
+    # record every timing event once so its CUDA handle exists before capture
+    with torch.cuda.stream(stream):
+        for r in range(R):
+            run_step(cases, sets[r])
+            for a, b in ev[r] + [step_ev[r]]:
+                a.record(stream)
+                b.record(stream)
+    torch.cuda.synchronize()
+    graphs = []
+    use_graph = not args.no_graph
+    if use_graph:
+        for r in range(R):
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph, stream=stream):
+                ext.record(step_ev[r][0], stream)
+                run_step(cases, sets[r], ev[r], ext, stream)
+                ext.record(step_ev[r][1], stream)
+            graphs.append(gph)
+    torch.cuda.synchronize()
+
+    def one(i):
+        r = i % R
+        if use_graph:
+            graphs[r].replay()
+        else:
+            with torch.cuda.stream(stream):
+                step_ev[r][0].record(stream)
+                for k, (c, d) in enumerate(zip(cases, sets[r])):
+                    sten.sparsify_grouped_nm(d["W"], c.n, c.m, c.g, values=d["values"], idx=d["idx"])
+                    ev[r][k][0].record(stream)
+                    sten.spmm_grouped_nm(d["values"], d["idx"], d["B"], c.n, c.m, c.g, out=d["C"],
+                                         plan=d["plan"])
+                    ev[r][k][1].record(stream)
+                step_ev[r][1].record(stream)
+
+    for i in range(args.warmup):
+        one(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local_rank) if (rank == 0 and not args.profile) else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms, spmm_ms = [], [[] for _ in cases]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(args.steps):
+        one(i)
+        # read back the events of this set before it is replayed again
+        if (i + 1) % R == 0 or i == args.steps - 1:
+            torch.cuda.synchronize()
+            for j in range(i - (i % R), i + 1):
+                r = j % R
+                step_ms.append(step_ev[r][0].elapsed_time(step_ev[r][1]))
+                for k in range(len(cases)):
+                    spmm_ms[k].append(ev[r][k][0].elapsed_time(ev[r][k][1]))
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    loop_ms = t0.elapsed_time(t1)
+    total_ms = float(sum(step_ms))
+    # max over ranks
+    tt = torch.tensor([total_ms], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+    flops_step = sum(eff_flops(c) for c in cases)
+    value = flops_step * world * args.steps / (total_ms * 1e-3) / 1e9
+
+    # dominant kernel: the SpMM (fp32 -> CUDA-core FFMA bound, bf16 -> tensor / HBM)
+    spmm_total_ms = sum(sum(x) for x in spmm_ms)
+    spmm_nz = sum(nz_flops(c) for c in cases) * args.steps
+    spmm_bytes_tot = sum(spmm_bytes(c) for c in cases) * args.steps
+    launches_per_step = sum(1 + sten.launch_count(d["plan"]) for d in sets[0])
+    peaks = load_peaks()
+    if dtype == "f32":
+        peak = peaks["fp32_tflops"]
+        achieved = spmm_nz / (spmm_total_ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4), "traffic": peaks.get("traffic_spmm"),
+                "peak_source": peaks["fp32_source"], "kernel": "spmm_simt_kernel (CUDA-core FFMA)"}
+    else:
+        t_roof = sum(max(nz_flops(c) / (peaks["bf16_tflops"] * 1e12), spmm_bytes(c) / (peaks["hbm_gbs"] * 1e9))
+                     for c in cases) * args.steps
+        frac = t_roof / (spmm_total_ms * 1e-3)
+        hbm_bound = sum(spmm_bytes(c) / (peaks["hbm_gbs"] * 1e9) for c in cases) >= sum(
+            nz_flops(c) / (peaks["bf16_tflops"] * 1e12) for c in cases)
+        if hbm_bound:
+            achieved = spmm_bytes_tot / (spmm_total_ms * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": round(frac, 4), "traffic": peaks.get("traffic_spmm")}
+        else:
+            achieved = spmm_nz / (spmm_total_ms * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peaks["bf16_tflops"],
+                    "unit": "TFLOP/s", "frac": round(frac, 4), "traffic": peaks.get("traffic_spmm")}
+        roof["kernel"] = "spmm (bf16)"
+    per_case = []
+    for k, c in enumerate(cases):
+        t = sum(spmm_ms[k]) / len(spmm_ms[k])
+        per_case.append({"case": c.label(), "plan": sets[0][k]["plan"].as_dict(), "spmm_us": round(t * 1e3, 2),
+                         "spmm_eff_gflops": round(eff_flops(c) / (t * 1e-3) / 1e9, 1),
+                         "spmm_nz_tflops": round(nz_flops(c) / (t * 1e-3) / 1e12, 3)})
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic (seeded N(0,0.02^2) weights, N(0,1) activations)",
+        "config": {"workload": CONFIG_NAMES[cfg], "baseline_config_index": cfg, "g": g,
+                   "cases": [c.label() for c in cases], "tokens_per_gpu": cases[0].N,
+                   "parallelism": "dp%d (token-sharded, weight replicated)" % world,
+                   "l2": "rotating %d input sets, %.0f MB > 3x L2 (%.0f MB)" % (R, R * set_bytes / 2 ** 20,
+                                                                            l2 / 2 ** 20),
+                   "cuda_graph": use_graph, "step": "sparsify (a1-a3) + SpMM (a5-a7) per case"},
+        "roofline": roof,
+        "spmm_only": {"value": round(sum(eff_flops(c) for c in cases) * args.steps / (spmm_total_ms * 1e-3) / 1e9, 2),
+                      "unit": UNIT, "share_of_step": round(spmm_total_ms / sum(step_ms), 4)},
+        "per_case": per_case,
+        "gpu_launches": launches_per_step * args.steps,
+        "loop_ms_device": round(loop_ms, 3),
+    }
+    if clocks:
+        out["clocks"] = clocks
+    return out, cases, host, dtype, g
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback (B200_PROFILING.md)"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            mp = json.load(f)
+        peaks.update({"hbm_gbs": mp.get("hbm_gbs", 6650.0), "bf16_tflops": mp.get("bf16_tflops", 1590.0),
+                      "src": "measured (MEASURED_PEAKS.json)"})
+        sm_mhz = mp.get("sm_max_mhz", 1965.0)
+    else:
+        sm_mhz = 1965.0
+    # FP32 CUDA-core peak derived from unit counts and clock
+    peaks["fp32_tflops"] = NUM_SMS * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    peaks["fp32_source"] = "derived: 148 SM x 128 FP32 lanes x 2 flop x %.0f MHz" % sm_mhz
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            peaks["traffic_spmm"] = json.load(f).get("spmm_dram_bytes_per_launch")
+    return peaks
+
+
+# ------------------------------------------------------------------------------------------------
+# e2e through the public C ABI with host buffers
+# ------------------------------------------------------------------------------------------------
+def bench_e2e(cases, host, dtype, steps, device):
+    import torch
+    from paper_2304_07613_b200 import sten
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    bufs = []
+    h2d = d2h = 0
+    for c, (W, B) in zip(cases, host):
+        Wh = torch.from_numpy(W.view(np.int16) if dtype == "bf16" else W)
+        Bh = torch.from_numpy(B.view(np.int16) if dtype == "bf16" else B)
+        if dtype == "bf16":
+            Wh, Bh = Wh.view(torch.bfloat16), Bh.view(torch.bfloat16)
+        Wh, Bh = Wh.pin_memory(), Bh.pin_memory()
+        Ch = torch.empty((c.M, c.N), dtype=tdt).pin_memory()
+        ws = torch.empty(sten.sparse_linear_host_workspace_size(c.n, c.m, c.g, c.M, c.Kp, c.N, tdt, tdt),
+                         dtype=torch.uint8, device=device)
+        bufs.append((Wh, Bh, Ch, ws))
+        h2d += Wh.numel() * Wh.element_size() + Bh.numel() * Bh.element_size()
+        d2h += Ch.numel() * Ch.element_size()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for c, (Wh, Bh, Ch, ws) in zip(cases, bufs):
+            sten.sparse_linear_host(Wh, Bh, c.n, c.m, c.g, Ch, ws)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    val = sum(eff_flops(c) for c in cases) * steps / (ms * 1e-3) / 1e9
+    return {"value": round(val, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": round(ms / steps, 4),
+            "path": "sten_sparse_linear_host (pinned host W,B -> H2D -> sparsify -> SpMM -> D2H C)"}
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline leg and --impl reference)
+# ------------------------------------------------------------------------------------------------
+def oracle_step_time(cases, host, sample_cols, nthreads):
+    """Time the oracle on one step: sparsify every full W, SpMM on `sample_cols` columns.
+    Returns (seconds extrapolated to the full step, seconds spent, sparsify s, spmm s per column)."""
+    import oracle
+    t_sp = t_mm_col = t_full = t_spent = 0.0
+    for c, (W, B) in zip(cases, host):
+        t0 = time.perf_counter()
+        v, i = oracle.sparsify(W, c.n, c.m, c.g)
+        t1 = time.perf_counter()
+        ns = min(sample_cols, c.N)
+        Bs = np.ascontiguousarray(B[:, :ns])
+        oracle.spmm(v, i, Bs, c.n, c.m, c.g, nthreads=nthreads, with_bound=False)
+        t2 = time.perf_counter()
+        t_sp += t1 - t0
+        t_mm_col += (t2 - t1) / ns
+        t_full += (t1 - t0) + (t2 - t1) * (c.N / ns)
+        t_spent += t2 - t0
+    return t_full, t_spent, t_sp, t_mm_col
+
+
+def calibrate_cols(cases, host, nthreads, budget_s):
+    """Largest column sample (multiple of 8, <= N) whose sampled step costs about budget_s."""
+    _, _, t_sp, t_col = oracle_step_time(cases, host, 8, nthreads)
+    cols = int(max(8.0, (budget_s - t_sp) / max(t_col, 1e-9)))
+    return max(8, min(cases[0].N, cols // 8 * 8))
+
+
+def cpu_baseline(cases, host, budget_s=15.0):
+    import oracle
+    oracle.build()
+    nt = cores()
+    cols = calibrate_cols(cases, host, nt, budget_s)
+    t_full, t_spent, _, _ = oracle_step_time(cases, host, cols, nt)
+    val = sum(eff_flops(c) for c in cases) / t_full / 1e9
+    return {"value": round(val, 4), "unit": UNIT, "cores": nt, "kind": "oracle",
+            "sample": "one step: oracle sparsify of every full W + oracle SpMM (fp64, %d threads) on the first %d "
+                      "token columns of each case, extrapolated linearly to all %d tokens; %.1f s of CPU work"
+                      % (nt, cols, cases[0].N, t_spent)}
+
+
+def bench_reference(args, rank, world):
+    cfg = args.config
+    dtype, g = default_dtype_g(cfg)
+    dtype = args.dtype or dtype
+    g = args.g or g
+    cases = cases_for(cfg, g, dtype)
+    host = []
+    for ci, c in enumerate(cases):
+        host.append((synthetic.weights(c.M, c.K, seed=1234 + ci, dtype=c.dtype, k_pad=c.k_pad),
+                     synthetic.activations(c.K, c.N, seed=1234 + ci, dtype=c.dtype, k_pad=c.k_pad)))
+    import oracle
+    oracle.build()
+    nt = cores()
+    # size the per-step column sample so the whole run stays within ~3 minutes
+    total_steps = args.steps + args.warmup
+    cols = calibrate_cols(cases, host, nt, budget_s=min(20.0, 150.0 / max(1, total_steps)))
+    for _ in range(args.warmup):
+        oracle_step_time(cases, host, cols, nt)
+    ts, spent = [], 0.0
+    for _ in range(args.steps):
+        t_full, t_sp, _, _ = oracle_step_time(cases, host, cols, nt)
+        ts.append(t_full)
+        spent += t_sp
+    tot = float(sum(ts))
+    val = sum(eff_flops(c) for c in cases) * args.steps / tot / 1e9
+    sample = ("each step: oracle sparsify of every full W + oracle SpMM (fp64, %d threads) on the first %d token "
+              "columns per case, time extrapolated linearly to all %d tokens (%.1f s CPU work in the timed steps)"
+              % (nt, cols, cases[0].N, spent))
+    return {
+        "metric": METRIC, "value": round(val, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "config": {"workload": CONFIG_NAMES[cfg], "baseline_config_index": cfg, "g": g,
+                   "cases": [c.label() for c in cases]},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": nt, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        out = bench_reference(args, rank, world)
+        line = json.dumps(out)
+        print(line, flush=True)
+        if args.out:
+            with open(args.out, "a") as f:
+                f.write(line + "\n")
+        return 0
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out, cases, host, dtype, g = bench_sten(args, rank, world, local_rank)
+    if not args.profile:
+        if not args.no_e2e:
+            e2e = bench_e2e(cases, host, dtype, max(3, min(args.steps, 10)), torch.device("cuda", local_rank))
+            if world > 1:
+                t = torch.tensor([e2e["value"]], dtype=torch.float64, device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MIN)
+                e2e["value"] = round(float(t.item()) * world, 2)
+            out["e2e"] = e2e
+        if rank == 0 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(cases, host)
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = json.dumps(out)
+        print(line, flush=True)
+        if args.out:
+            with open(args.out, "a") as f:
+                f.write(line + "\n")
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

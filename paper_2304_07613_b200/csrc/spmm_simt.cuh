@@ -2,64 +2,116 @@
 //
 // Computes C = densify(values, idx) x B  (the sparse-dense GEMM of STen,
 // PAPER.md:527-538, Fig. 5), redesigned for sm_100a:
-//   (1) the paper's "load sparse values, broadcast into vector registers"
-//       becomes a shared-memory broadcast: the g values of one kept k of a
-//       group are stored contiguously ([k'][g]) so one LDS.128 feeds a warp;
-//   (2) "indirect loads from specific rows of B" become indirect reads of a
-//       B K-slab staged in shared memory by cp.async (16-byte LDGSTS,
-//       double-buffered); the row offset of every kept k is precomputed per
-//       slab, so the inner loop has no index arithmetic;
-//   (3) "FMA" is FFMA into an RG x TN register tile per lane: RG rows of one
-//       group (which share every kept k) x TN columns.  Each staged B element
-//       read from shared memory feeds RG FMAs.
+//   (1) "load sparse values, broadcast into vector registers" -> the values
+//       tile of a K-slab is staged in shared memory ([row][k'], cp.async) and a
+//       warp reads 4 consecutive k' of one row with one broadcast LDS.128, so
+//       the RG rows of a sub-block cost RG wavefronts per 4 kept k;
+//   (2) "indirect loads from specific rows of B" -> indirect LDS.128 reads of
+//       a B K-slab staged in shared memory by a STAGES-deep cp.async ring; the
+//       byte offset of every kept k of the warp's sub-blocks is rebuilt
+//       warp-privately once per slab, so the inner loop is LDS + FFMA only;
+//   (3) "FMA" -> FFMA into an RG x TN register tile per lane and sub-block
+//       (RG rows of one group share every kept k, so each B element read from
+//       shared memory feeds RG FMAs).
 //
-// CTA = 8 warps; warp w owns SUB sub-blocks of RG rows (each inside one group
-// since RG | g; sub-blocks of different groups gather different B rows) and all
-// BN = 32*TN columns of the tile, i.e. SUB*RG*TN fp32 accumulators per lane.
-// BM = 8*SUB*RG rows per CTA sets the reuse of every staged B element across
-// the CTA (BM*n/m rows use it), which keeps L2->SM traffic at 4/(BM*n/m) bytes
-// per FMA for fp32.  Lane l owns the columns
-// {j*32*EV + l*EV + e}, EV = 16/sizeof(T), so every shared/global vector access
-// of a warp covers 512 contiguous bytes (conflict-free, coalesced).
+// CTA = WARPS warps; warp w owns SUB sub-blocks of RG rows (RG | g) and all
+// BN = 32*TN columns of the tile.  Lane l owns columns {j*32*EV + l*EV + e},
+// EV = 16/sizeof(T): every vector access of a warp covers 512 contiguous bytes.
+// BM = WARPS*SUB*RG rows per CTA sets the reuse of every staged B element
+// (BM*n/m rows use it): L2->SM traffic is sizeof(T)/(BM*n/m) bytes per FMA.
 //
-// Split-K: the kept-k range of every row is cut into `split` contiguous parts
-// (fixed by the plan, never by N); part p is computed by blockIdx.z == p into a
-// private fp32 workspace slice and a second kernel adds the parts in order
-// 0..split-1 -- so the summation order of a column is independent of N tiling.
+// Split-K (plan.split_k = S > 1): the S CTAs of one output tile form a thread-
+// block cluster (1,1,S); CTA z computes the partial sum of the z-th contiguous
+// range of m-blocks, parks it in its shared memory, and after a cluster
+// barrier every CTA reduces 1/S of the tile by reading the S partials over
+// DSMEM in the fixed order z = 0..S-1.  No workspace, no second launch, and
+// the per-column summation order depends only on (K, n, m, plan) -- never on N.
 #pragma once
+#include <cuda.h>
 #include "common.cuh"
 
 namespace sten {
 
-template <typename TAB, int RG, int TN, int SUB>
+// Arguments common to the SpMM kernels.
+struct SpmmArgs {
+    const void* values;
+    const uint8_t* idx;
+    const void* B;
+    void* C;
+    int64_t M, K, N, ldb, ldc;
+    int n, m, g;
+    int64_t Kp;            // kept per row
+    int64_t KB;            // m-blocks per row
+    int64_t kb_per_split;  // m-blocks per split-K part (multiple of the slab)
+    int split;             // S (cluster z extent)
+    int kbs;               // m-blocks per K-slab
+    bool c_vec;            // C base/ldc allow vector stores
+    bool v_tma;            // values tile staged by a 3-D TMA box into [ksp/KU][BM][KU]
+    bool v_async;          // else: values rows vector-aligned -> 16B (fp32) / 8B (bf16) cp.async
+    int64_t idx_bytes;     // size of the idx array (bounds the aligned-down idx word loads)
+};
+
+template <typename TAB, int RG, int TN, int SUB, int WARPS>
 struct SimtCfg {
-    static constexpr int kWarps = 8;
-    static constexpr int kThreads = kWarps * 32;
-    static constexpr int kEV = 16 / int(sizeof(TAB));    // elements per 16-byte vector
-    static constexpr int kChunks = TN / kEV;               // 16-byte chunks per lane
-    static constexpr int kBN = 32 * TN;                    // CTA columns
-    static constexpr int kSubs = kWarps * SUB;             // RG-row sub-blocks per CTA
-    static constexpr int kBM = kSubs * RG;                 // CTA rows
-    static constexpr int kRGP = RG <= 1 ? 1 : RG <= 2 ? 2 : RG <= 4 ? 4 : 8;   // padded
-    static constexpr int kSlabRows = sizeof(TAB) == 4 ? 32 : 64;   // target BK
-    static constexpr int kMaxKS = kSlabRows;               // kept k per slab <= BK
+    static constexpr int kWarps = WARPS;
+    static constexpr int kThreads = WARPS * 32;
+    static constexpr int kEV = 16 / int(sizeof(TAB));      // elements per 16-byte vector
+    static constexpr int kChunks = TN / kEV;                 // 16-byte chunks per lane and B row
+    static constexpr int kBN = 32 * TN;                      // CTA columns
+    static constexpr int kSubs = WARPS * SUB;                // RG-row sub-blocks per CTA
+    static constexpr int kBM = kSubs * RG;                   // CTA rows
+    static constexpr int kStages = 3;
+    static constexpr int kKU = RG <= 4 ? 4 : 2;             // kept k per inner-loop step
     static_assert(TN % kEV == 0, "TN must be a multiple of the vector width");
 };
 
-// Number of m-blocks per slab for a given m.
-template <typename TAB>
-__host__ __device__ constexpr int simt_blocks_per_slab(int m) {
-    return (sizeof(TAB) == 4 ? 32 : 64) / m > 0 ? (sizeof(TAB) == 4 ? 32 : 64) / m : 1;
+__host__ __device__ inline int gcd_int(int a, int b) {
+    while (b) { int t = a % b; a = b; b = t; }
+    return a;
 }
 
-template <typename TAB, int RG, int TN, int SUB>
-__host__ __device__ constexpr size_t simt_smem_bytes(int m) {
-    using Cfg = SimtCfg<TAB, RG, TN, SUB>;
-    const int bk = simt_blocks_per_slab<TAB>(m) * m;
-    return 2 * (size_t(bk) * Cfg::kBN * sizeof(TAB)                       // B slabs
-                + size_t(Cfg::kSubs) * Cfg::kMaxKS * Cfg::kRGP * 4        // values (fp32)
-                + size_t(Cfg::kSubs) * Cfg::kMaxKS * 4);                  // row offsets
+// m-blocks per K-slab: a multiple of 4/gcd(n,4) (so kept-per-slab is a multiple
+// of 4) with at most `target_rows` B rows (at least one such multiple).
+__host__ __device__ inline int simt_kbs(int n, int m, int target_rows) {
+    const int q = 4 / gcd_int(n, 4);
+    int kbs = q;
+    while ((kbs + q) * m <= target_rows) kbs += q;
+    return kbs;
 }
+
+template <typename TAB>
+__host__ __device__ constexpr int simt_target_rows() { return sizeof(TAB) == 4 ? 32 : 64; }
+
+__host__ __device__ constexpr size_t align128(size_t x) { return (x + 127) & ~size_t(127); }
+
+// Shared-memory layout (byte offsets from the dynamic smem base):
+//   [0, hdr)            mbarriers full[ST] | per-sub idx base (int64) | block-row table [ksp]
+//   stage s             B slab [bk][BN] | values [BM][ksp] | idx words [NSUB][iwords]
+//   offs                warp-private row addresses [NSUB][ksp]
+//   zero                one zero B row (target of padded kept slots)
+//   split-K partial tile [BM][BN] fp32 parked at `hdr` after the main loop
+template <typename TAB, int RG, int TN, int SUB, int WARPS>
+struct SimtSmem {
+    using Cfg = SimtCfg<TAB, RG, TN, SUB, WARPS>;
+    size_t hdr, b_stage, v_stage, i_stage, stage, stages, offs, zero, total;
+    int bk, ksp, iwords;
+    __host__ __device__ SimtSmem(int kbs, int n, int m) {
+        bk = kbs * m;
+        ksp = kbs * n;                                                   // multiple of 4
+        iwords = ksp / 4 + 1;                                            // covers a 3-byte misalignment
+        hdr = align128(Cfg::kStages * 8 + size_t(Cfg::kSubs) * 8 + size_t(ksp) * 4);
+        b_stage = align128(size_t(bk) * Cfg::kBN * sizeof(TAB));
+        v_stage = align128(size_t(Cfg::kBM) * ksp * sizeof(TAB));
+        i_stage = align128(size_t(Cfg::kSubs) * iwords * 4);
+        stage = b_stage + v_stage + i_stage;
+        stages = hdr;
+        offs = hdr + Cfg::kStages * stage;
+        zero = align128(offs + size_t(Cfg::kSubs) * ksp * 4);
+        const size_t pipe = zero + Cfg::kBN * sizeof(TAB);
+        const size_t tile = hdr + size_t(Cfg::kBM) * Cfg::kBN * 4;
+        total = pipe > tile ? pipe : tile;
+    }
+};
 
 template <int EV>
 STEN_DEVICE_INLINE void unpack(const float4& raw, float (&b)[EV]) {
@@ -111,94 +163,163 @@ STEN_DEVICE_INLINE void store_out(TC* __restrict__ C, int64_t ldc, int64_t row, 
         if (col + e < N) p[e] = from_f32<TC>(v[e]);
 }
 
-// Arguments common to the SpMM kernels.
-struct SpmmArgs {
-    const void* values;
-    const uint8_t* idx;
-    const void* B;
-    void* C;            // final output (split == 1) or fp32 workspace [split][M][N]
-    int64_t M, K, N, ldb, ldc;
-    int n, m, g;
-    int64_t Kp;         // kept per row
-    int64_t KB;         // m-blocks per row
-    int64_t kb_per_split;   // m-blocks per split-K part
-    bool c_vec;         // C base/ldc allow vector stores
-};
+// ---- thread-block cluster helpers (split-K reduction over DSMEM) ------------------------------
+STEN_DEVICE_INLINE void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+STEN_DEVICE_INLINE uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+STEN_DEVICE_INLINE uint32_t map_cluster(uint32_t smem_addr, uint32_t rank) {
+    uint32_t d;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(d) : "r"(smem_addr), "r"(rank));
+    return d;
+}
+STEN_DEVICE_INLINE float4 ld_dsmem128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr));
+    return v;
+}
 
-template <typename TAB, typename TC, int RG, int TN, int SUB>
-__global__ void __launch_bounds__(256, 1)
-spmm_simt_kernel(const SpmmArgs a) {
-    using Cfg = SimtCfg<TAB, RG, TN, SUB>;
+// After every CTA of the cluster parked its fp32 partial tile [BM][BN] at the
+// start of its shared memory: reduce 1/S of the tile over DSMEM in the fixed
+// order z = 0..S-1 and store it to C.
+template <typename TC, int BM, int BN, int NT>
+STEN_DEVICE_INLINE void cluster_reduce_store(unsigned char* tile_smem, const SpmmArgs& a, int64_t m0, int64_t n0) {
+    cluster_sync_all();
+    const uint32_t S = uint32_t(a.split);
+    const uint32_t me = cluster_ctarank();
+    constexpr int E4 = BM * BN / 4;
+    const int e_begin = int(uint64_t(E4) * me / S), e_end = int(uint64_t(E4) * (me + 1) / S);
+    const uint32_t base = smem_u32(tile_smem);
+    TC* C = static_cast<TC*>(a.C);
+    for (int e = e_begin + int(threadIdx.x); e < e_end; e += NT) {
+        const uint32_t off = uint32_t(e) * 16u;
+        float4 s = ld_dsmem128(map_cluster(base + off, 0));
+        for (uint32_t z = 1; z < S; ++z) {
+            const float4 t = ld_dsmem128(map_cluster(base + off, z));
+            s.x = __fadd_rn(s.x, t.x); s.y = __fadd_rn(s.y, t.y);
+            s.z = __fadd_rn(s.z, t.z); s.w = __fadd_rn(s.w, t.w);
+        }
+        const int row = (e * 4) / BN, col = (e * 4) % BN;
+        const int64_t gr = m0 + row, gc = n0 + col;
+        if (gr < a.M && gc < a.N) {
+            const float v[4] = {s.x, s.y, s.z, s.w};
+            store_out<TC>(C, a.ldc, gr, gc, a.N, v, 4, a.c_vec);
+        }
+    }
+    cluster_sync_all();                     // keep every partial alive until all reads are done
+}
+
+template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && RG * TN * SUB <= 64) ? 2 : 1)
+spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmV) {
+    using Cfg = SimtCfg<TAB, RG, TN, SUB, WARPS>;
     constexpr int EV = Cfg::kEV;
-    constexpr int RGP = Cfg::kRGP;
     constexpr int BN = Cfg::kBN;
     constexpr int BM = Cfg::kBM;
     constexpr int NSUB = Cfg::kSubs;
-    constexpr int MAXKS = Cfg::kMaxKS;
+    constexpr int NT = Cfg::kThreads;
+    constexpr int ST = Cfg::kStages;
+    constexpr int ROWB = BN * int(sizeof(TAB));              // bytes per staged B row
+    constexpr int KU = Cfg::kKU;                             // kept k per inner step
 
     extern __shared__ __align__(128) unsigned char smem[];
-    const int kbs = simt_blocks_per_slab<TAB>(a.m);             // m-blocks per slab
-    const int bk = kbs * a.m;                                    // B rows per slab
-    const size_t b_stage = size_t(bk) * BN * sizeof(TAB);
-    unsigned char* sB[2] = {smem, smem + b_stage};
-    float* sV[2];
-    int* sO[2];
-    {
-        unsigned char* p = smem + 2 * b_stage;
-        sV[0] = reinterpret_cast<float*>(p); p += NSUB * MAXKS * RGP * 4;
-        sV[1] = reinterpret_cast<float*>(p); p += NSUB * MAXKS * RGP * 4;
-        sO[0] = reinterpret_cast<int*>(p);   p += NSUB * MAXKS * 4;
-        sO[1] = reinterpret_cast<int*>(p);
-    }
+    const int n = a.n, m = a.m, kbs = a.kbs;
+    const SimtSmem<TAB, RG, TN, SUB, WARPS> L(kbs, n, m);
+    const int ksp = L.ksp, iwords = L.iwords;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    int64_t* gbase = reinterpret_cast<int64_t*>(smem + ST * 8);          // idx row base of each sub-block
+    int* blkrow = reinterpret_cast<int*>(smem + ST * 8 + NSUB * 8);      // (kk / n) * m
+    int* sOff = reinterpret_cast<int*>(smem + L.offs);
+    const uint32_t zero_row = smem_u32(smem + L.zero);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int64_t n0 = int64_t(blockIdx.x) * BN;
     const int64_t m0 = int64_t(blockIdx.y) * BM;
-    const int part = blockIdx.z;
-    const int64_t kb_begin = int64_t(part) * a.kb_per_split;
-    const int64_t kb_end = min(a.KB, kb_begin + a.kb_per_split);
-    const int64_t nslabs = kb_end > kb_begin ? (kb_end - kb_begin + kbs - 1) / kbs : 0;
+    const int64_t kb_begin = int64_t(blockIdx.z) * a.kb_per_split;
+    const int64_t kb_end = min64(a.KB, kb_begin + a.kb_per_split);
+    const int nslabs = kb_end > kb_begin ? int((kb_end - kb_begin + kbs - 1) / kbs) : 0;
 
     const TAB* __restrict__ V = static_cast<const TAB*>(a.values);
-    const TAB* __restrict__ Bm = static_cast<const TAB*>(a.B);
-    const int n = a.n;
+    auto sB = [&](int buf) { return smem + L.stages + size_t(buf) * L.stage; };
+    auto sV = [&](int buf) { return smem + L.stages + size_t(buf) * L.stage + L.b_stage; };
+    auto sI = [&](int buf) { return smem + L.stages + size_t(buf) * L.stage + L.b_stage + L.v_stage; };
+    const uint32_t v_bytes = a.v_tma ? uint32_t(BM * ksp * sizeof(TAB)) : 0u;
+    const uint32_t tx_bytes = uint32_t(L.bk) * ROWB + v_bytes;
 
-    auto stage = [&](int64_t slab, int buf) {
-        const int64_t kb0 = kb_begin + slab * kbs;
-        const int nkb = int(min64(kbs, kb_end - kb0));
-        const int rows = nkb * a.m;
-        // B slab rows [kb0*m, kb0*m + rows) x columns [n0, n0 + BN): 16-byte cp.async
-        constexpr int CPR = BN / EV;    // chunks per slab row
-        for (int c = tid; c < rows * CPR; c += Cfg::kThreads) {
-            const int kr = c / CPR, cc = c - kr * CPR;
-            const int64_t col = n0 + int64_t(cc) * EV;
-            const int64_t krow = kb0 * a.m + kr;
-            const int bytes = int(max64(0, min64(EV, a.N - col))) * int(sizeof(TAB));
-            const TAB* src = bytes > 0 ? Bm + krow * a.ldb + col : Bm;
-            cp_async16(sB[buf] + (size_t(kr) * BN + cc * EV) * sizeof(TAB), src, bytes);
+    // ---- one-time setup: barriers, per-sub idx bases, block-row table, zero row ----
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    for (int sb = tid; sb < NSUB; sb += NT) {
+        const int64_t row = m0 + int64_t(sb) * RG;
+        gbase[sb] = row < a.M ? (row / a.g) * a.KB * n : int64_t(-1);
+    }
+    for (int kk = tid; kk < ksp; kk += NT) blkrow[kk] = (kk / n) * m;
+    for (int e = tid; e < BN * int(sizeof(TAB)) / 4; e += NT) reinterpret_cast<uint32_t*>(smem + L.zero)[e] = 0u;
+    __syncthreads();
+
+    // Issue the loads of slab `s` into buffer `buf`: B (and values) by TMA from thread 0,
+    // the rest by cp.async (one commit group per slab).
+    auto issue = [&](int s, int buf) {
+        if (s < nslabs) {
+            const int64_t kb0 = kb_begin + int64_t(s) * kbs;
+            const int nkb = int(min64(kbs, kb_end - kb0));
+            const int ks = nkb * n;
+            if (tid == 0) {
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx(&full[buf], tx_bytes);
+                tma_load_2d(sB(buf), &tmB, &full[buf], int(n0), int(kb0 * m));
+                if (a.v_tma) tma_load_3d(sV(buf), &tmV, &full[buf], 0, int(m0), int(kb0 * n / KU));
+            }
+            if (!a.v_tma) {
+                // values tile in k-group-major layout [ksp/KU][BM][KU] (zero beyond ks and beyond M)
+                for (int r = warp; r < BM; r += WARPS) {
+                    const int64_t row = m0 + r;
+                    const TAB* src_row = V + row * a.Kp + kb0 * n;
+                    if (a.v_async) {
+                        for (int kg = lane; kg < ksp / KU; kg += 32) {
+                            const int k0 = kg * KU;
+                            const int bytes = (row < a.M) ? max(0, min(KU, ks - k0)) * int(sizeof(TAB)) : 0;
+                            unsigned char* dst = sV(buf) + (size_t(kg) * BM + r) * KU * sizeof(TAB);
+                            const TAB* src = bytes > 0 ? src_row + k0 : V;
+                            if constexpr (KU * sizeof(TAB) == 16) cp_async16(dst, src, bytes);
+                            else if constexpr (KU * sizeof(TAB) == 8) cp_async8(dst, src, bytes);
+                            else cp_async4(dst, src, bytes);
+                        }
+                    } else if constexpr (sizeof(TAB) == 4) {
+                        for (int kk = lane; kk < ksp; kk += 32) {
+                            const int bytes = (row < a.M && kk < ks) ? 4 : 0;
+                            cp_async4(sV(buf) + ((size_t(kk / KU) * BM + r) * KU + kk % KU) * 4, bytes ? src_row + kk : V,
+                                      bytes);
+                        }
+                    } else {
+                        for (int kk = lane; kk < ksp; kk += 32)
+                            reinterpret_cast<TAB*>(sV(buf))[(size_t(kk / KU) * BM + r) * KU + kk % KU] =
+                                (row < a.M && kk < ks) ? src_row[kk] : TAB(0);
+                    }
+                }
+            }
+            // idx: the aligned 4-byte words covering [start, start + ks) of each sub-block's group
+            for (int sb = warp; sb < NSUB; sb += WARPS) {
+                const int64_t gb = gbase[sb];
+                const int64_t start = gb + kb0 * n;
+                for (int w = lane; w < iwords; w += 32) {
+                    const int64_t woff = (start & ~int64_t(3)) + 4 * w;
+                    const int bytes = gb >= 0 ? int(max64(0, min64(4, min64(a.idx_bytes, start + ks) - woff))) : 0;
+                    cp_async4(sI(buf) + (size_t(sb) * iwords + w) * 4, bytes ? a.idx + woff : a.idx, bytes);
+                }
+            }
         }
         cp_async_commit();
-        // values (transposed to [sub][k'][RGP], widened to fp32) and row byte offsets
-        const int ks = nkb * n;
-        for (int e = tid; e < BM * ks; e += Cfg::kThreads) {
-            const int wr = e / ks, kk = e - wr * ks;
-            const int64_t row = m0 + wr;
-            float v = 0.0f;
-            if (row < a.M) v = to_f32(V[row * a.Kp + kb0 * n + kk]);
-            sV[buf][((wr / RG) * MAXKS + kk) * RGP + (wr % RG)] = v;
-        }
-        for (int e = tid; e < NSUB * ks; e += Cfg::kThreads) {
-            const int sb = e / ks, kk = e - sb * ks;
-            const int64_t row = m0 + int64_t(sb) * RG;
-            int off = 0;
-            if (row < a.M) {
-                const int64_t grp = row / a.g;
-                const int j = a.idx[(grp * a.KB + kb0) * n + kk];   // block kb0 + kk/n, slot kk%n
-                off = ((kk / n) * a.m + j) * BN * int(sizeof(TAB));
-            }
-            sO[buf][sb * MAXKS + kk] = off;
-        }
     };
 
     float acc[SUB][RG][TN];
@@ -209,90 +330,127 @@ spmm_simt_kernel(const SpmmArgs a) {
 #pragma unroll
             for (int c = 0; c < TN; ++c) acc[q][r][c] = 0.0f;
 
-    // warp w owns sub-blocks [w*SUB, (w+1)*SUB); sub-blocks past M are skipped
     const int sub0 = warp * SUB;
     const bool warp_active = (m0 + int64_t(sub0) * RG) < a.M;
-    if (nslabs > 0) stage(0, 0);
-    for (int64_t s = 0; s < nslabs; ++s) {
-        const int buf = int(s & 1);
-        if (s + 1 < nslabs) {
-            stage(s + 1, buf ^ 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
+
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) issue(s, s);
+    for (int s = 0; s < nslabs; ++s) {
+        const int buf = s % ST;
+        cp_async_wait<ST - 2>();
+        mbar_wait(&full[buf], uint32_t((s / ST) & 1));
+        __syncthreads();                     // slab s visible; everyone is done with slab s-1
+        issue(s + ST - 1, (s + ST - 1) % ST);
         if (warp_active) {
-            const int64_t kb0 = kb_begin + s * kbs;
+            const int64_t kb0 = kb_begin + int64_t(s) * kbs;
             const int ks = int(min64(kbs, kb_end - kb0)) * n;
-            const unsigned char* bs = sB[buf] + size_t(lane) * EV * sizeof(TAB);
-            const float* vs = sV[buf] + size_t(sub0) * MAXKS * RGP;
-            const int* os = sO[buf] + sub0 * MAXKS;
-#pragma unroll 2
-            for (int kk = 0; kk < ks; ++kk) {
+            const int ks4 = (ks + 3) & ~3;
+            // warp-private shared addresses of the staged B rows of every kept k of my sub-blocks
+            // (padded slots point at the zero row)
+            // warp-private shared addresses of the staged B rows of every kept k of my sub-blocks,
+            // k-group-major [ksp/KU][NSUB][KU] (padded slots point at the zero row)
+            const uint32_t bbase = smem_u32(sB(buf));
+#pragma unroll
+            for (int q = 0; q < SUB; ++q) {
+                const int64_t start = gbase[sub0 + q] + kb0 * n;
+                const uint8_t* ib = sI(buf) + size_t(sub0 + q) * iwords * 4 + int(start & 3);
+                for (int kk = lane; kk < ksp; kk += 32)
+                    sOff[(kk / KU * NSUB + sub0 + q) * KU + kk % KU] =
+                        kk < ks ? int(bbase) + (blkrow[kk] + ib[kk]) * ROWB : int(zero_row);
+            }
+            __syncwarp();
+            const uint32_t lane_off = uint32_t(lane) * 16u;
+            const unsigned char* vbase = sV(buf) + size_t(sub0) * RG * KU * sizeof(TAB);
+            const int* obase = sOff + sub0 * KU;
+            for (int kg = 0; kg < ks4 / KU; ++kg) {
+                const unsigned char* vg = vbase + size_t(kg) * BM * KU * sizeof(TAB);
+                const int* og = obase + kg * NSUB * KU;
 #pragma unroll
                 for (int q = 0; q < SUB; ++q) {
-                    const int off = os[q * MAXKS + kk];
-                    float v[RGP];
-                    const float* vp = vs + (q * MAXKS + kk) * RGP;
-                    if constexpr (RGP >= 4) {
-#pragma unroll
-                        for (int u = 0; u < RGP / 4; ++u) {
-                            const float4 t = lds128(vp + 4 * u);
-                            v[4 * u] = t.x; v[4 * u + 1] = t.y; v[4 * u + 2] = t.z; v[4 * u + 3] = t.w;
-                        }
+                    int offs[KU];
+                    if constexpr (KU == 4) {
+                        const int4 o = *reinterpret_cast<const int4*>(og + q * KU);
+                        offs[0] = o.x; offs[1] = o.y; offs[2] = o.z; offs[3] = o.w;
                     } else {
+                        const int2 o = *reinterpret_cast<const int2*>(og + q * KU);
+                        offs[0] = o.x; offs[1] = o.y;
+                    }
+                    float v[RG][KU];
 #pragma unroll
-                        for (int u = 0; u < RGP; ++u) v[u] = vp[u];
+                    for (int r = 0; r < RG; ++r) {
+                        const unsigned char* vp = vg + size_t(q * RG + r) * KU * sizeof(TAB);
+                        if constexpr (sizeof(TAB) == 4 && KU == 4) {
+                            const float4 t = *reinterpret_cast<const float4*>(vp);
+                            v[r][0] = t.x; v[r][1] = t.y; v[r][2] = t.z; v[r][3] = t.w;
+                        } else if constexpr (sizeof(TAB) == 4) {
+                            const float2 t = *reinterpret_cast<const float2*>(vp);
+                            v[r][0] = t.x; v[r][1] = t.y;
+                        } else if constexpr (KU == 4) {
+                            const uint2 t = *reinterpret_cast<const uint2*>(vp);
+                            v[r][0] = __uint_as_float(t.x << 16); v[r][1] = __uint_as_float(t.x & 0xffff0000u);
+                            v[r][2] = __uint_as_float(t.y << 16); v[r][3] = __uint_as_float(t.y & 0xffff0000u);
+                        } else {
+                            const uint32_t t = *reinterpret_cast<const uint32_t*>(vp);
+                            v[r][0] = __uint_as_float(t << 16); v[r][1] = __uint_as_float(t & 0xffff0000u);
+                        }
                     }
 #pragma unroll
-                    for (int j = 0; j < Cfg::kChunks; ++j) {
-                        float b[EV];
-                        unpack<EV>(lds128(bs + off + size_t(j) * 32 * EV * sizeof(TAB)), b);
+                    for (int t = 0; t < KU; ++t) {
+                        const uint32_t ba = uint32_t(offs[t]) + lane_off;
 #pragma unroll
-                        for (int r = 0; r < RG; ++r)
+                        for (int j = 0; j < Cfg::kChunks; ++j) {
+                            float b[EV];
+                            unpack<EV>(lds128_addr(ba + uint32_t(j) * 512u), b);
 #pragma unroll
-                            for (int e = 0; e < EV; ++e)
-                                acc[q][r][j * EV + e] = fmaf(v[r], b[e], acc[q][r][j * EV + e]);
+                            for (int r = 0; r < RG; ++r)
+#pragma unroll
+                                for (int e = 0; e < EV; e += 2) {
+                                    float2& c2 = *reinterpret_cast<float2*>(&acc[q][r][j * EV + e]);
+                                    c2 = __ffma2_rn(make_float2(v[r][t], v[r][t]), make_float2(b[e], b[e + 1]), c2);
+                                }
+                        }
                     }
                 }
             }
         }
-        __syncthreads();
     }
+    cp_async_wait<0>();
 
-    if (!warp_active) return;
-    const bool final_out = gridDim.z == 1;
+    if (a.split == 1) {
+        if (!warp_active) return;
+        TC* C = static_cast<TC*>(a.C);
 #pragma unroll
-    for (int q = 0; q < SUB; ++q) {
+        for (int q = 0; q < SUB; ++q)
+#pragma unroll
+            for (int r = 0; r < RG; ++r) {
+                const int64_t row = m0 + int64_t(sub0 + q) * RG + r;
+                if (row >= a.M) continue;
+#pragma unroll
+                for (int j = 0; j < Cfg::kChunks; ++j)
+                    store_out<TC>(C, a.ldc, row, n0 + int64_t(j) * 32 * EV + lane * EV, a.N, &acc[q][r][j * EV],
+                                  EV, a.c_vec);
+            }
+        return;
+    }
+    // split-K: park the partial tile [BM][BN] (fp32) after the header, reduce over the cluster
+    __syncthreads();
+    float* tile = reinterpret_cast<float*>(smem + L.hdr);
+#pragma unroll
+    for (int q = 0; q < SUB; ++q)
 #pragma unroll
         for (int r = 0; r < RG; ++r) {
-            const int64_t row = m0 + int64_t(sub0 + q) * RG + r;
-            if (row >= a.M) continue;
+            const int row = (sub0 + q) * RG + r;
 #pragma unroll
-            for (int j = 0; j < Cfg::kChunks; ++j) {
-                const int64_t col = n0 + int64_t(j) * 32 * EV + lane * EV;
-                if (final_out)
-                    store_out<TC>(static_cast<TC*>(a.C), a.ldc, row, col, a.N, &acc[q][r][j * EV], EV, a.c_vec);
-                else
-                    store_out<float>(static_cast<float*>(a.C) + int64_t(part) * a.M * a.N, a.N, row, col, a.N,
-                                     &acc[q][r][j * EV], EV, (a.N % 4) == 0);
-            }
+            for (int j = 0; j < Cfg::kChunks; ++j)
+#pragma unroll
+                for (int e4 = 0; e4 < EV; e4 += 4) {
+                    const int col = j * 32 * EV + lane * EV + e4;
+                    *reinterpret_cast<float4*>(tile + size_t(row) * BN + col) =
+                        make_float4(acc[q][r][j * EV + e4], acc[q][r][j * EV + e4 + 1], acc[q][r][j * EV + e4 + 2],
+                                    acc[q][r][j * EV + e4 + 3]);
+                }
         }
-    }
-}
-
-// Ordered reduction of split-K partials: C = ((p0 + p1) + p2) + ...
-template <typename TC>
-__global__ void __launch_bounds__(256)
-splitk_reduce_kernel(const float* __restrict__ parts, int split, int64_t M, int64_t N,
-                     TC* __restrict__ C, int64_t ldc) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= M * N) return;
-    const int64_t r = i / N, c = i - r * N;
-    float s = parts[i];
-    for (int p = 1; p < split; ++p) s = __fadd_rn(s, parts[int64_t(p) * M * N + i]);
-    C[r * ldc + c] = from_f32<TC>(s);
+    cluster_reduce_store<TC, BM, BN, NT>(smem + L.hdr, a, m0, n0);
 }
 
 }  // namespace sten

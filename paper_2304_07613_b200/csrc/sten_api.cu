@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include "common.cuh"
+#include "tma_host.h"
 #include "sparsify.cuh"
 #include "spmm_simt.cuh"
 #include "spmm_mma.cuh"
@@ -102,51 +103,96 @@ int simt_rows_per_warp(int g) {
     return 1;
 }
 
-// SIMT tile variants (plan.tile): 1 = TN8/SUB1, 2 = TN8/SUB2, 3 = TN8/SUB4, 4 = TN4/SUB8.
-struct SimtTile { int tn, sub; };
-constexpr SimtTile kSimtTiles[5] = {{0, 0}, {8, 1}, {8, 2}, {8, 4}, {4, 8}};
+// SIMT tile variants (plan.tile), every one with 64 fp32 accumulators per lane:
+//   1: 8 warps,  TN = 8, BM = 64,  BN = 256 (fp32) / 256 (bf16)  -- 2 CTAs / SM
+//   2: 16 warps, TN = 8, BM = 128, BN = 256                      -- 1 CTA / SM
+//   3: 16 warps, TN = 4, BM = 256, BN = 128 (fp32 only)          -- 1 CTA / SM
+struct SimtTile { int warps, tn, bm; };
+constexpr SimtTile kSimtTiles[4] = {{0, 0, 0}, {8, 8, 64}, {16, 8, 128}, {16, 4, 256}};
+constexpr int kMaxSplit = 8;              // portable thread-block cluster size
 
-inline bool simt_tile_ok(int tile, int rg) {
-    if (tile < 1 || tile > 4) return false;
-    return rg * kSimtTiles[tile].tn * kSimtTiles[tile].sub <= 128;    // accumulators per lane
+inline bool simt_tile_ok(int tile, sten_dtype ab) {
+    if (tile < 1 || tile > 3) return false;
+    return !(tile == 3 && ab == STEN_BF16);
 }
 
-template <typename TAB, typename TC, int RG, int TN, int SUB>
-sten_status launch_simt_cfg(const SpmmArgs& a, int split, cudaStream_t st) {
-    if constexpr (RG * TN * SUB > 128 || TN < 16 / int(sizeof(TAB))) {
-        return STEN_ERR_UNSUPPORTED;
-    } else {
-        using Cfg = SimtCfg<TAB, RG, TN, SUB>;
-        const size_t smem = simt_smem_bytes<TAB, RG, TN, SUB>(a.m);
-        auto kern = spmm_simt_kernel<TAB, TC, RG, TN, SUB>;
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
-            return STEN_ERR_CUDA;
-        dim3 grid(unsigned((a.N + Cfg::kBN - 1) / Cfg::kBN), unsigned((a.M + Cfg::kBM - 1) / Cfg::kBM),
-                  unsigned(split));
-        kern<<<grid, Cfg::kThreads, smem, st>>>(a);
-        return last_cuda();
-    }
+// m-blocks per slab for the SIMT kernel
+int simt_slab_blocks(sten_nmg f, sten_dtype ab) {
+    return simt_kbs(f.n, f.m, ab == STEN_F32 ? simt_target_rows<float>() : simt_target_rows<bf16_t>());
+}
+
+template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS>
+sten_status launch_simt_cfg(SpmmArgs a, cudaStream_t st) {
+    using Cfg = SimtCfg<TAB, RG, TN, SUB, WARPS>;
+    const SimtSmem<TAB, RG, TN, SUB, WARPS> L(a.kbs, a.n, a.m);
+    if (L.total > 227 * 1024) return STEN_ERR_UNSUPPORTED;
+    const CUtensorMapDataType tdt = sizeof(TAB) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    constexpr size_t s = sizeof(TAB);
+    CUtensorMap tmB, tmV;
+    memset(&tmB, 0, sizeof(tmB));
+    memset(&tmV, 0, sizeof(tmV));
+    if (!make_tmap_2d(&tmB, a.B, tdt, uint64_t(a.N), uint64_t(a.K), uint64_t(a.ldb) * s, Cfg::kBN, uint32_t(L.bk)))
+        return STEN_ERR_CUDA;
+    // values as a 3-D tensor {KU, M, Kp/KU} (strides Kp*s, KU*s) so the box lands as [ksp/KU][BM][KU];
+    // needs 16-byte inner boxes and strides, else the kernel stages values with cp.async
+    constexpr int KU = Cfg::kKU;
+    a.v_tma = KU * s == 16 && (size_t(a.Kp) * s) % 16 == 0 && aligned16(a.values) &&
+              make_tmap_3d(&tmV, a.values, tdt, uint64_t(KU), uint64_t(a.M), uint64_t(a.Kp / KU),
+                           uint64_t(a.Kp) * s, uint64_t(KU) * s, uint32_t(KU), Cfg::kBM, uint32_t(L.ksp / KU));
+    auto kern = spmm_simt_kernel<TAB, TC, RG, TN, SUB, WARPS>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total)) != cudaSuccess)
+        return STEN_ERR_CUDA;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned((a.N + Cfg::kBN - 1) / Cfg::kBN), unsigned((a.M + Cfg::kBM - 1) / Cfg::kBM),
+                       unsigned(a.split));
+    cfg.blockDim = dim3(Cfg::kThreads);
+    cfg.dynamicSmemBytes = L.total;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = unsigned(a.split);
+    cfg.attrs = attr;
+    cfg.numAttrs = a.split > 1 ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, kern, a, tmB, tmV) != cudaSuccess) return STEN_ERR_CUDA;
+    return last_cuda();
 }
 
 template <typename TAB, typename TC, int RG>
-sten_status launch_simt_rg(const SpmmArgs& a, int tile, int split, cudaStream_t st) {
+sten_status launch_simt_rg(const SpmmArgs& a, int tile, cudaStream_t st) {
+    constexpr int SUB8 = 8 / RG;                 // TN = 8: RG * 8 * SUB8 = 64 accumulators
     switch (tile) {
-        case 1: return launch_simt_cfg<TAB, TC, RG, 8, 1>(a, split, st);
-        case 2: return launch_simt_cfg<TAB, TC, RG, 8, 2>(a, split, st);
-        case 3: return launch_simt_cfg<TAB, TC, RG, 8, 4>(a, split, st);
-        case 4: return launch_simt_cfg<TAB, TC, RG, 4, 8>(a, split, st);
+        case 1: return launch_simt_cfg<TAB, TC, RG, 8, SUB8, 8>(a, st);
+        case 2: return launch_simt_cfg<TAB, TC, RG, 8, SUB8, 16>(a, st);
+        case 3:
+            if constexpr (sizeof(TAB) == 4) return launch_simt_cfg<TAB, TC, RG, 4, 2 * SUB8, 16>(a, st);
+            else return STEN_ERR_UNSUPPORTED;
     }
     return STEN_ERR_UNSUPPORTED;
 }
 
 template <typename TAB, typename TC>
-sten_status launch_simt(const SpmmArgs& a, int tile, int split, cudaStream_t st) {
+sten_status launch_simt(const SpmmArgs& a, int tile, cudaStream_t st) {
     switch (simt_rows_per_warp(a.g)) {
-        case 8: return launch_simt_rg<TAB, TC, 8>(a, tile, split, st);
-        case 4: return launch_simt_rg<TAB, TC, 4>(a, tile, split, st);
-        case 2: return launch_simt_rg<TAB, TC, 2>(a, tile, split, st);
-        default: return launch_simt_rg<TAB, TC, 1>(a, tile, split, st);
+        case 8: return launch_simt_rg<TAB, TC, 8>(a, tile, st);
+        case 4: return launch_simt_rg<TAB, TC, 4>(a, tile, st);
+        case 2: return launch_simt_rg<TAB, TC, 2>(a, tile, st);
+        default: return launch_simt_rg<TAB, TC, 1>(a, tile, st);
     }
+}
+
+// Ordered reduction of split-K partials (mma.sync path): C = ((p0 + p1) + p2) + ...
+template <typename TC>
+__global__ void __launch_bounds__(256)
+splitk_reduce_kernel(const float* __restrict__ parts, int split, int64_t M, int64_t N,
+                     TC* __restrict__ C, int64_t ldc) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= M * N) return;
+    const int64_t r = i / N, c = i - r * N;
+    float s = parts[i];
+    for (int p = 1; p < split; ++p) s = __fadd_rn(s, parts[int64_t(p) * M * N + i]);
+    C[r * ldc + c] = from_f32<TC>(s);
 }
 
 template <typename TC>
@@ -166,14 +212,15 @@ __global__ void zero_fill_kernel(TC* C, int64_t M, int64_t N, int64_t ldc) {
 
 constexpr int kNumSMs = 148;
 
-// Pick split_k for `tiles` output tiles over KB m-blocks: minimise
-// waves(S) * ceil(KB/S) * t_kb + reduce(S), with one resident CTA per SM.
-int choose_split(int64_t tiles, int64_t KB, double t_kb_clk, double reduce_clk_per_split) {
+// Pick split_k in [1, max_split] for `tiles` output tiles of `slots` resident CTAs
+// per wave over KB m-blocks: minimise waves(S) * ceil(KB/S) * t_kb + reduce(S).
+int choose_split(int64_t tiles, int64_t slots, int64_t KB, int max_split, double t_kb_clk,
+                 double reduce_clk) {
     int best = 1;
     double best_t = 1e300;
-    for (int S = 1; S <= 16 && S <= KB; ++S) {
-        const double waves = double((tiles * S + kNumSMs - 1) / kNumSMs);
-        const double t = waves * double((KB + S - 1) / S) * t_kb_clk + (S > 1 ? S * reduce_clk_per_split : 0.0);
+    for (int S = 1; S <= max_split && S <= KB; ++S) {
+        const double waves = double((tiles * S + slots - 1) / slots);
+        const double t = waves * double((KB + S - 1) / S) * t_kb_clk + (S > 1 ? reduce_clk : 0.0);
         if (t < best_t * 0.97) { best_t = t; best = S; }
     }
     return best;
@@ -192,23 +239,21 @@ sten_status plan_auto(sten_nmg f, sten_dtype ab, int64_t M, int64_t K, int64_t N
         const int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
         const double t_kb = double(bm * bn * f.n) / 512.0;      // clk per m-block per CTA (MMA-bound guess)
         const double red = double(M) * N * 8.0 / (kNumSMs * 40.0);
-        p->split_k = choose_split(tiles, KB, t_kb, red);
+        p->split_k = choose_split(tiles, kNumSMs, KB, 16, t_kb, red);
         return STEN_OK;
     }
     p->algo = STEN_ALGO_SIMT;
-    const int rg = simt_rows_per_warp(f.g);
+    // B-operand reuse: want BM * n/m >= 32 rows per staged B element (L2 traffic <= 1/8 B per FMA)
     int tile = 1;
-    for (int t = 1; t <= 3; ++t) {
-        if (!simt_tile_ok(t, rg)) break;
-        tile = t;
-        if (8.0 * kSimtTiles[t].sub * rg * d >= 32.0) break;
-    }
+    if (64.0 * d < 32.0) tile = 2;
+    if (128.0 * d < 32.0 && ab == STEN_F32) tile = 3;
     p->tile = tile;
-    const int64_t bm = 8 * kSimtTiles[tile].sub * rg, bn = 32 * kSimtTiles[tile].tn;
+    const int64_t bm = kSimtTiles[tile].bm, bn = 32 * kSimtTiles[tile].tn;
     const int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
-    const double t_kb = double(bm * bn * f.n) / 128.0;          // clk per m-block per CTA (FFMA-bound)
-    const double red = double(M) * N * 8.0 / (kNumSMs * 40.0);
-    p->split_k = choose_split(tiles, KB, t_kb, red);
+    const int64_t slots = kNumSMs * (tile == 1 ? 2 : 1);
+    const double t_kb = double(bm * bn * f.n) / (128.0 / (tile == 1 ? 2 : 1));  // clk per m-block per CTA
+    const double red = double(bm * bn * 4) / 20.0;                          // DSMEM bytes / (B/clk)
+    p->split_k = choose_split(tiles, slots, KB, kMaxSplit, t_kb, red);
     return STEN_OK;
 }
 
@@ -224,6 +269,7 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
     if ((M * K > 0 && (!values || !idx)) || (K * N > 0 && !B) || (M * N > 0 && !C)) return STEN_ERR_INVALID_ARG;
     const size_t sab = dt_size(ab_dt), sc = dt_size(c_dt);
     if (K * N > 0 && (!aligned16(B) || (ldb * int64_t(sab)) % 16 != 0)) return STEN_ERR_UNSUPPORTED;
+    if ((reinterpret_cast<uintptr_t>(idx) & 3u) != 0) return STEN_ERR_UNSUPPORTED;
     sten_spmm_plan plan;
     plan_auto(f, ab_dt, M, K, N, c_dt, &plan);
     if (plan_in) {
@@ -234,13 +280,14 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
         if (plan_in->tile > 0) plan.tile = plan_in->tile;
         if (plan_in->split_k > 0) plan.split_k = plan_in->split_k;
     }
-    if (plan.split_k < 1 || plan.split_k > 64) return STEN_ERR_UNSUPPORTED;
     if (plan.algo == STEN_ALGO_MMA_SYNC && (ab_dt != STEN_BF16 || !mma_supported(f.g)))
         return STEN_ERR_UNSUPPORTED;
     if (plan.algo != STEN_ALGO_SIMT && plan.algo != STEN_ALGO_MMA_SYNC) return STEN_ERR_UNSUPPORTED;
-    if (plan.algo == STEN_ALGO_SIMT && !simt_tile_ok(plan.tile, simt_rows_per_warp(f.g))) return STEN_ERR_UNSUPPORTED;
+    if (plan.algo == STEN_ALGO_SIMT && (!simt_tile_ok(plan.tile, ab_dt) || plan.split_k > kMaxSplit))
+        return STEN_ERR_UNSUPPORTED;
     if (plan.algo == STEN_ALGO_MMA_SYNC && !(plan.tile == 1 || (plan.tile == 2 && f.g % 16 == 0)))
         return STEN_ERR_UNSUPPORTED;
+    if (plan.split_k < 1 || plan.split_k > 64) return STEN_ERR_UNSUPPORTED;
     if (M == 0 || N == 0) return STEN_OK;
     if (K == 0) {
         if (c_dt == STEN_F32) zero_fill_kernel<float><<<grid1d(M * N), 256, 0, st>>>(static_cast<float*>(C), M, N, ldc);
@@ -249,28 +296,40 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
     }
 
     SpmmArgs a;
+    memset(&a, 0, sizeof(a));
     a.values = values; a.idx = idx; a.B = B; a.C = C;
     a.M = M; a.K = K; a.N = N; a.ldb = ldb; a.ldc = ldc;
     a.n = f.n; a.m = f.m; a.g = f.g;
     a.KB = K / f.m; a.Kp = a.KB * f.n;
-    const int split = int(plan.split_k > a.KB ? a.KB : plan.split_k);
-    a.kb_per_split = (a.KB + split - 1) / split;
     a.c_vec = aligned16(C) && (ldc * int64_t(sc)) % 16 == 0;
 
+    if (plan.algo == STEN_ALGO_SIMT) {
+        a.v_async = (a.Kp % 4 == 0) && ((reinterpret_cast<uintptr_t>(values) & (4 * sab - 1)) == 0);
+        a.idx_bytes = (M / f.g) * a.KB * f.n;
+        a.kbs = simt_slab_blocks(f, ab_dt);
+        // split-K parts are whole slabs; S = ceil(KB / per-part)
+        const int64_t slabs = (a.KB + a.kbs - 1) / a.kbs;
+        const int64_t per = (slabs + plan.split_k - 1) / plan.split_k;
+        a.kb_per_split = per * a.kbs;
+        a.split = int((a.KB + a.kb_per_split - 1) / a.kb_per_split);
+        if (ab_dt == STEN_F32) s = c_dt == STEN_F32 ? launch_simt<float, float>(a, plan.tile, st)
+                                                    : launch_simt<float, bf16_t>(a, plan.tile, st);
+        else s = c_dt == STEN_F32 ? launch_simt<bf16_t, float>(a, plan.tile, st)
+                                  : launch_simt<bf16_t, bf16_t>(a, plan.tile, st);
+        return s;
+    }
+
+    // mma.sync path: split-K partials through a stream-ordered workspace + ordered reduce
+    const int split = int(plan.split_k > a.KB ? a.KB : plan.split_k);
+    a.kb_per_split = (a.KB + split - 1) / split;
+    a.split = split;
     float* parts = nullptr;
     if (split > 1) {
         if (cudaMallocAsync(reinterpret_cast<void**>(&parts), size_t(split) * M * N * 4, st) != cudaSuccess)
             return STEN_ERR_CUDA;
         a.C = parts;
     }
-    if (plan.algo == STEN_ALGO_SIMT) {
-        if (ab_dt == STEN_F32) s = c_dt == STEN_F32 ? launch_simt<float, float>(a, plan.tile, split, st)
-                                                    : launch_simt<float, bf16_t>(a, plan.tile, split, st);
-        else s = c_dt == STEN_F32 ? launch_simt<bf16_t, float>(a, plan.tile, split, st)
-                                  : launch_simt<bf16_t, bf16_t>(a, plan.tile, split, st);
-    } else {
-        s = c_dt == STEN_F32 ? launch_mma<float>(a, plan.tile, split, st) : launch_mma<bf16_t>(a, plan.tile, split, st);
-    }
+    s = c_dt == STEN_F32 ? launch_mma<float>(a, plan.tile, split, st) : launch_mma<bf16_t>(a, plan.tile, split, st);
     if (split > 1) {
         if (s == STEN_OK)
             s = c_dt == STEN_F32 ? launch_reduce<float>(parts, split, M, N, C, ldc, st)
@@ -420,7 +479,8 @@ const char* sten_algo_name(int32_t algo) {
 
 int32_t sten_spmm_launch_count(const sten_spmm_plan* plan) {
     if (!plan) return 1;
-    return plan->split_k > 1 ? 2 : 1;
+    // SIMT reduces split-K partials inside the kernel (cluster DSMEM); mma.sync adds a reduce launch
+    return (plan->algo == STEN_ALGO_MMA_SYNC && plan->split_k > 1) ? 2 : 1;
 }
 
 int32_t sten_version(void) { return 1; }
