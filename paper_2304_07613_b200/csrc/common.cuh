@@ -47,6 +47,11 @@ STEN_DEVICE_INLINE void cp_async4(void* smem, const void* gmem, int src_bytes) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(smem)),
                  "l"(gmem), "r"(src_bytes));
 }
+// the mbarrier receives one arrive when all prior cp.async of this thread have landed
+// (.noinc: that arrive counts against the barrier's initial arrival count)
+STEN_DEVICE_INLINE void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 STEN_DEVICE_INLINE void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 STEN_DEVICE_INLINE void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -82,6 +87,13 @@ STEN_DEVICE_INLINE void fence_proxy_async_smem() {
 STEN_DEVICE_INLINE void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
+}
+STEN_DEVICE_INLINE void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+STEN_DEVICE_INLINE void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 STEN_DEVICE_INLINE void mbar_wait(uint64_t* bar, uint32_t phase) {
     asm volatile(

@@ -32,6 +32,22 @@
 
 namespace sten {
 
+// Optional per-CTA phase timestamps (debug builds with -DSTEN_TIMING only; tools/phase_timing.py).
+#ifdef STEN_TIMING
+__device__ unsigned long long g_sten_timing[16384][8];
+#define STEN_TSTAMP(i)                                                                                    \
+    do {                                                                                                  \
+        if (threadIdx.x == 0) {                                                                           \
+            unsigned long long t_;                                                                        \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
+            const unsigned cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);          \
+            if (cta_ < 16384) g_sten_timing[cta_][i] = t_;                                               \
+        }                                                                                                 \
+    } while (0)
+#else
+#define STEN_TSTAMP(i) do { } while (0)
+#endif
+
 // Arguments common to the SpMM kernels.
 struct SpmmArgs {
     const void* values;
@@ -51,14 +67,15 @@ struct SpmmArgs {
     int64_t idx_bytes;     // size of the idx array (bounds the aligned-down idx word loads)
 };
 
+// WARPS = warps per CTA: WARPS-1 consumer warps + 1 producer warp.
 template <typename TAB, int RG, int TN, int SUB, int WARPS>
 struct SimtCfg {
-    static constexpr int kWarps = WARPS;
+    static constexpr int kWarps = WARPS - 1;                 // consumer warps
     static constexpr int kThreads = WARPS * 32;
     static constexpr int kEV = 16 / int(sizeof(TAB));      // elements per 16-byte vector
     static constexpr int kChunks = TN / kEV;                 // 16-byte chunks per lane and B row
     static constexpr int kBN = 32 * TN;                      // CTA columns
-    static constexpr int kSubs = WARPS * SUB;                // RG-row sub-blocks per CTA
+    static constexpr int kSubs = (WARPS - 1) * SUB;          // RG-row sub-blocks per CTA
     static constexpr int kBM = kSubs * RG;                   // CTA rows
     static constexpr int kStages = 3;
     static constexpr int kKU = RG <= 4 ? 4 : 2;             // kept k per inner-loop step
@@ -90,27 +107,32 @@ __host__ __device__ constexpr size_t align128(size_t x) { return (x + 127) & ~si
 //   offs                warp-private row addresses [NSUB][ksp]
 //   zero                one zero B row (target of padded kept slots)
 //   split-K partial tile [BM][BN] fp32 parked at `hdr` after the main loop
-template <typename TAB, int RG, int TN, int SUB, int WARPS>
-struct SimtSmem {
-    using Cfg = SimtCfg<TAB, RG, TN, SUB, WARPS>;
+struct SimtLayout {
     size_t hdr, b_stage, v_stage, i_stage, stage, stages, offs, zero, total;
     int bk, ksp, iwords;
-    __host__ __device__ SimtSmem(int kbs, int n, int m) {
+    __host__ __device__ SimtLayout(int bm, int bn, int nsub, int esz, int nstages, int kbs, int n, int m) {
         bk = kbs * m;
         ksp = kbs * n;                                                   // multiple of 4
         iwords = ksp / 4 + 1;                                            // covers a 3-byte misalignment
-        hdr = align128(Cfg::kStages * 8 + size_t(Cfg::kSubs) * 8 + size_t(ksp) * 4);
-        b_stage = align128(size_t(bk) * Cfg::kBN * sizeof(TAB));
-        v_stage = align128(size_t(Cfg::kBM) * ksp * sizeof(TAB));
-        i_stage = align128(size_t(Cfg::kSubs) * iwords * 4);
+        hdr = align128(size_t(nstages) * 16 + size_t(nsub) * 8);         // full/empty mbarriers, idx bases
+        b_stage = align128(size_t(bk) * bn * esz);
+        v_stage = align128(size_t(bm) * ksp * esz);
+        i_stage = align128(size_t(nsub) * iwords * 4);
         stage = b_stage + v_stage + i_stage;
         stages = hdr;
-        offs = hdr + Cfg::kStages * stage;
-        zero = align128(offs + size_t(Cfg::kSubs) * ksp * 4);
-        const size_t pipe = zero + Cfg::kBN * sizeof(TAB);
-        const size_t tile = hdr + size_t(Cfg::kBM) * Cfg::kBN * 4;
+        offs = hdr + size_t(nstages) * stage;                            // warp-private row addresses
+        zero = align128(offs + size_t(nsub) * ksp * 4);
+        const size_t pipe = zero + size_t(bn) * esz;
+        const size_t tile = hdr + size_t(bm) * bn * 4;
         total = pipe > tile ? pipe : tile;
     }
+};
+
+template <typename TAB, int RG, int TN, int SUB, int WARPS>
+struct SimtSmem : SimtLayout {
+    using Cfg = SimtCfg<TAB, RG, TN, SUB, WARPS>;
+    __host__ __device__ SimtSmem(int kbs, int n, int m)
+        : SimtLayout(Cfg::kBM, Cfg::kBN, Cfg::kSubs, int(sizeof(TAB)), Cfg::kStages, kbs, n, m) {}
 };
 
 template <int EV>
@@ -216,15 +238,25 @@ STEN_DEVICE_INLINE void cluster_reduce_store(unsigned char* tile_smem, const Spm
     cluster_sync_all();                     // keep every partial alive until all reads are done
 }
 
+// Warp-specialised pipeline: warps 0..WARPS-2 consume (LDS + FFMA2), warp WARPS-1 produces.
+// Per stage the producer (1) waits until every consumer warp released the buffer
+// (empty mbarrier), (2) arms the full mbarrier with the TMA byte count and issues the
+// TMA loads of the B slab (and of the values tile when it is TMA-able), (3) issues
+// cp.async for the raw idx words (and the values otherwise), and (4) hands their
+// completion to the full mbarrier (cp.async.mbarrier.arrive.noinc, one per lane).
+// A consumer waits on the full barrier, turns its sub-blocks' idx bytes into shared
+// addresses of staged B rows (warp-private), runs the LDS/FFMA2 loop and arrives on
+// the empty barrier.  No CTA-wide barrier per slab.
 template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && RG * TN * SUB <= 64) ? 2 : 1)
+__global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1)
 spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmV) {
     using Cfg = SimtCfg<TAB, RG, TN, SUB, WARPS>;
     constexpr int EV = Cfg::kEV;
     constexpr int BN = Cfg::kBN;
     constexpr int BM = Cfg::kBM;
     constexpr int NSUB = Cfg::kSubs;
-    constexpr int NT = Cfg::kThreads;
+    constexpr int NT = WARPS * 32;
+    constexpr int CW = WARPS - 1;                            // consumer warps
     constexpr int ST = Cfg::kStages;
     constexpr int ROWB = BN * int(sizeof(TAB));              // bytes per staged B row
     constexpr int KU = Cfg::kKU;                             // kept k per inner step
@@ -234,10 +266,8 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
     const SimtSmem<TAB, RG, TN, SUB, WARPS> L(kbs, n, m);
     const int ksp = L.ksp, iwords = L.iwords;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-    int64_t* gbase = reinterpret_cast<int64_t*>(smem + ST * 8);          // idx row base of each sub-block
-    int* blkrow = reinterpret_cast<int*>(smem + ST * 8 + NSUB * 8);      // (kk / n) * m
-    int* sOff = reinterpret_cast<int*>(smem + L.offs);
-    const uint32_t zero_row = smem_u32(smem + L.zero);
+    uint64_t* empty = full + ST;
+    int64_t* gbase = reinterpret_cast<int64_t*>(smem + ST * 16);         // idx row base of each sub-block
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -247,80 +277,25 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
     const int64_t kb_end = min64(a.KB, kb_begin + a.kb_per_split);
     const int nslabs = kb_end > kb_begin ? int((kb_end - kb_begin + kbs - 1) / kbs) : 0;
 
-    const TAB* __restrict__ V = static_cast<const TAB*>(a.values);
     auto sB = [&](int buf) { return smem + L.stages + size_t(buf) * L.stage; };
     auto sV = [&](int buf) { return smem + L.stages + size_t(buf) * L.stage + L.b_stage; };
     auto sI = [&](int buf) { return smem + L.stages + size_t(buf) * L.stage + L.b_stage + L.v_stage; };
-    const uint32_t v_bytes = a.v_tma ? uint32_t(BM * ksp * sizeof(TAB)) : 0u;
-    const uint32_t tx_bytes = uint32_t(L.bk) * ROWB + v_bytes;
 
-    // ---- one-time setup: barriers, per-sub idx bases, block-row table, zero row ----
+    STEN_TSTAMP(0);
     if (tid == 0) {
-        for (int s = 0; s < ST; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&full[s], 32);          // one cp.async-completion arrive per producer lane
+            mbar_init(&empty[s], CW);
+        }
         fence_mbar_init();
     }
     for (int sb = tid; sb < NSUB; sb += NT) {
         const int64_t row = m0 + int64_t(sb) * RG;
         gbase[sb] = row < a.M ? (row / a.g) * a.KB * n : int64_t(-1);
     }
-    for (int kk = tid; kk < ksp; kk += NT) blkrow[kk] = (kk / n) * m;
     for (int e = tid; e < BN * int(sizeof(TAB)) / 4; e += NT) reinterpret_cast<uint32_t*>(smem + L.zero)[e] = 0u;
     __syncthreads();
-
-    // Issue the loads of slab `s` into buffer `buf`: B (and values) by TMA from thread 0,
-    // the rest by cp.async (one commit group per slab).
-    auto issue = [&](int s, int buf) {
-        if (s < nslabs) {
-            const int64_t kb0 = kb_begin + int64_t(s) * kbs;
-            const int nkb = int(min64(kbs, kb_end - kb0));
-            const int ks = nkb * n;
-            if (tid == 0) {
-                fence_proxy_async_smem();
-                mbar_arrive_expect_tx(&full[buf], tx_bytes);
-                tma_load_2d(sB(buf), &tmB, &full[buf], int(n0), int(kb0 * m));
-                if (a.v_tma) tma_load_3d(sV(buf), &tmV, &full[buf], 0, int(m0), int(kb0 * n / KU));
-            }
-            if (!a.v_tma) {
-                // values tile in k-group-major layout [ksp/KU][BM][KU] (zero beyond ks and beyond M)
-                for (int r = warp; r < BM; r += WARPS) {
-                    const int64_t row = m0 + r;
-                    const TAB* src_row = V + row * a.Kp + kb0 * n;
-                    if (a.v_async) {
-                        for (int kg = lane; kg < ksp / KU; kg += 32) {
-                            const int k0 = kg * KU;
-                            const int bytes = (row < a.M) ? max(0, min(KU, ks - k0)) * int(sizeof(TAB)) : 0;
-                            unsigned char* dst = sV(buf) + (size_t(kg) * BM + r) * KU * sizeof(TAB);
-                            const TAB* src = bytes > 0 ? src_row + k0 : V;
-                            if constexpr (KU * sizeof(TAB) == 16) cp_async16(dst, src, bytes);
-                            else if constexpr (KU * sizeof(TAB) == 8) cp_async8(dst, src, bytes);
-                            else cp_async4(dst, src, bytes);
-                        }
-                    } else if constexpr (sizeof(TAB) == 4) {
-                        for (int kk = lane; kk < ksp; kk += 32) {
-                            const int bytes = (row < a.M && kk < ks) ? 4 : 0;
-                            cp_async4(sV(buf) + ((size_t(kk / KU) * BM + r) * KU + kk % KU) * 4, bytes ? src_row + kk : V,
-                                      bytes);
-                        }
-                    } else {
-                        for (int kk = lane; kk < ksp; kk += 32)
-                            reinterpret_cast<TAB*>(sV(buf))[(size_t(kk / KU) * BM + r) * KU + kk % KU] =
-                                (row < a.M && kk < ks) ? src_row[kk] : TAB(0);
-                    }
-                }
-            }
-            // idx: the aligned 4-byte words covering [start, start + ks) of each sub-block's group
-            for (int sb = warp; sb < NSUB; sb += WARPS) {
-                const int64_t gb = gbase[sb];
-                const int64_t start = gb + kb0 * n;
-                for (int w = lane; w < iwords; w += 32) {
-                    const int64_t woff = (start & ~int64_t(3)) + 4 * w;
-                    const int bytes = gb >= 0 ? int(max64(0, min64(4, min64(a.idx_bytes, start + ks) - woff))) : 0;
-                    cp_async4(sI(buf) + (size_t(sb) * iwords + w) * 4, bytes ? a.idx + woff : a.idx, bytes);
-                }
-            }
-        }
-        cp_async_commit();
-    };
+    STEN_TSTAMP(1);
 
     float acc[SUB][RG][TN];
 #pragma unroll
@@ -329,128 +304,189 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
         for (int r = 0; r < RG; ++r)
 #pragma unroll
             for (int c = 0; c < TN; ++c) acc[q][r][c] = 0.0f;
-
     const int sub0 = warp * SUB;
-    const bool warp_active = (m0 + int64_t(sub0) * RG) < a.M;
 
-#pragma unroll
-    for (int s = 0; s < ST - 1; ++s) issue(s, s);
-    for (int s = 0; s < nslabs; ++s) {
-        const int buf = s % ST;
-        cp_async_wait<ST - 2>();
-        mbar_wait(&full[buf], uint32_t((s / ST) & 1));
-        __syncthreads();                     // slab s visible; everyone is done with slab s-1
-        issue(s + ST - 1, (s + ST - 1) % ST);
-        if (warp_active) {
+    if (warp == CW) {
+        // ======================= producer warp =======================
+        const TAB* __restrict__ V = static_cast<const TAB*>(a.values);
+        const uint32_t v_bytes = a.v_tma ? uint32_t(BM * ksp * sizeof(TAB)) : 0u;
+        const uint32_t tx_bytes = uint32_t(L.bk) * ROWB + v_bytes;
+        for (int s = 0; s < nslabs; ++s) {
+            const int buf = s % ST;
+            if (s >= ST) mbar_wait(&empty[buf], uint32_t(((s / ST) - 1) & 1));
             const int64_t kb0 = kb_begin + int64_t(s) * kbs;
-            const int ks = int(min64(kbs, kb_end - kb0)) * n;
-            const int ks4 = (ks + 3) & ~3;
-            // warp-private shared addresses of the staged B rows of every kept k of my sub-blocks
-            // (padded slots point at the zero row)
-            // warp-private shared addresses of the staged B rows of every kept k of my sub-blocks,
-            // k-group-major [ksp/KU][NSUB][KU] (padded slots point at the zero row)
-            const uint32_t bbase = smem_u32(sB(buf));
-#pragma unroll
-            for (int q = 0; q < SUB; ++q) {
-                const int64_t start = gbase[sub0 + q] + kb0 * n;
-                const uint8_t* ib = sI(buf) + size_t(sub0 + q) * iwords * 4 + int(start & 3);
-                for (int kk = lane; kk < ksp; kk += 32)
-                    sOff[(kk / KU * NSUB + sub0 + q) * KU + kk % KU] =
-                        kk < ks ? int(bbase) + (blkrow[kk] + ib[kk]) * ROWB : int(zero_row);
+            const int nkb = int(min64(kbs, kb_end - kb0));
+            const int ks = nkb * n;
+            if (lane == 0) {
+                fence_proxy_async_smem();
+                mbar_expect_tx(&full[buf], tx_bytes);
+                tma_load_2d(sB(buf), &tmB, &full[buf], int(n0), int(kb0 * m));
+                if (a.v_tma) tma_load_3d(sV(buf), &tmV, &full[buf], 0, int(m0), int(kb0 * n / KU));
             }
-            __syncwarp();
-            const uint32_t lane_off = uint32_t(lane) * 16u;
-            const unsigned char* vbase = sV(buf) + size_t(sub0) * RG * KU * sizeof(TAB);
-            const int* obase = sOff + sub0 * KU;
-            for (int kg = 0; kg < ks4 / KU; ++kg) {
-                const unsigned char* vg = vbase + size_t(kg) * BM * KU * sizeof(TAB);
-                const int* og = obase + kg * NSUB * KU;
+            if (!a.v_tma) {
+                // values tile in k-group-major layout [ksp/KU][BM][KU] (zero beyond ks and beyond M)
+                if (a.v_async) {
+                    const int ngr = ksp / KU;
+                    for (int e = lane; e < BM * ngr; e += 32) {
+                        const int r = e / ngr, kg = e - r * ngr;
+                        const int64_t row = m0 + r;
+                        const int k0 = kg * KU;
+                        const int bytes = (row < a.M) ? max(0, min(KU, ks - k0)) * int(sizeof(TAB)) : 0;
+                        unsigned char* dst = sV(buf) + (size_t(kg) * BM + r) * KU * sizeof(TAB);
+                        const TAB* src = bytes > 0 ? V + row * a.Kp + kb0 * n + k0 : V;
+                        if constexpr (KU * sizeof(TAB) == 16) cp_async16(dst, src, bytes);
+                        else if constexpr (KU * sizeof(TAB) == 8) cp_async8(dst, src, bytes);
+                        else cp_async4(dst, src, bytes);
+                    }
+                } else if constexpr (sizeof(TAB) == 4) {
+                    for (int e = lane; e < BM * ksp; e += 32) {
+                        const int r = e / ksp, kk = e - r * ksp;
+                        const int64_t row = m0 + r;
+                        const int bytes = (row < a.M && kk < ks) ? 4 : 0;
+                        cp_async4(sV(buf) + ((size_t(kk / KU) * BM + r) * KU + kk % KU) * 4,
+                                  bytes ? V + row * a.Kp + kb0 * n + kk : V, bytes);
+                    }
+                } else {
+                    for (int e = lane; e < BM * ksp; e += 32) {
+                        const int r = e / ksp, kk = e - r * ksp;
+                        const int64_t row = m0 + r;
+                        reinterpret_cast<TAB*>(sV(buf))[(size_t(kk / KU) * BM + r) * KU + kk % KU] =
+                            (row < a.M && kk < ks) ? V[row * a.Kp + kb0 * n + kk] : TAB(0);
+                    }
+                }
+            }
+            // raw idx: the aligned 4-byte words covering [start, start + ks) of each sub-block's group
+            for (int e = lane; e < NSUB * iwords; e += 32) {
+                const int sb = e / iwords, w = e - sb * iwords;
+                const int64_t gb = gbase[sb];
+                const int64_t start = gb + kb0 * n;
+                const int64_t woff = (start & ~int64_t(3)) + 4 * w;
+                const int bytes = gb >= 0 ? int(max64(0, min64(4, min64(a.idx_bytes, start + ks) - woff))) : 0;
+                cp_async4(sI(buf) + size_t(e) * 4, bytes ? a.idx + woff : a.idx, bytes);
+            }
+            cp_async_mbar_arrive_noinc(&full[buf]);
+        }
+        if (a.split == 1) return;
+    } else {
+        // ======================= consumer warps =======================
+        const bool warp_active = (m0 + int64_t(sub0) * RG) < a.M;
+        const uint32_t lane_off = uint32_t(lane) * 16u;
+        const uint32_t zero_row = smem_u32(smem + L.zero);
+        int* wo = reinterpret_cast<int*>(smem + L.offs) + sub0 * ksp;   // [ksp/KU][SUB][KU], warp-private
+        for (int s = 0; s < nslabs; ++s) {
+            const int buf = s % ST;
+            mbar_wait(&full[buf], uint32_t((s / ST) & 1));
+            if (s == 0) STEN_TSTAMP(2);
+            if (warp_active) {
+                const int64_t kb0 = kb_begin + int64_t(s) * kbs;
+                const int ks = int(min64(kbs, kb_end - kb0)) * n;
+                const int nkg = (ks + KU - 1) / KU;
+                const uint32_t bbase = smem_u32(sB(buf));
 #pragma unroll
                 for (int q = 0; q < SUB; ++q) {
-                    int offs[KU];
-                    if constexpr (KU == 4) {
-                        const int4 o = *reinterpret_cast<const int4*>(og + q * KU);
-                        offs[0] = o.x; offs[1] = o.y; offs[2] = o.z; offs[3] = o.w;
-                    } else {
-                        const int2 o = *reinterpret_cast<const int2*>(og + q * KU);
-                        offs[0] = o.x; offs[1] = o.y;
-                    }
-                    float v[RG][KU];
+                    const int64_t start = gbase[sub0 + q] + kb0 * n;
+                    const uint8_t* ib = sI(buf) + size_t(sub0 + q) * iwords * 4 + int(start & 3);
+                    for (int kk = lane; kk < ksp; kk += 32)
+                        wo[((kk / KU) * SUB + q) * KU + kk % KU] =
+                            kk < ks ? int(bbase) + ((kk / n) * m + ib[kk]) * ROWB : int(zero_row);
+                }
+                __syncwarp();
+                const unsigned char* vbase = sV(buf) + size_t(sub0) * RG * KU * sizeof(TAB);
+                for (int kg = 0; kg < nkg; ++kg) {
+                    const unsigned char* vg = vbase + size_t(kg) * BM * KU * sizeof(TAB);
+                    const int* og = wo + kg * SUB * KU;
 #pragma unroll
-                    for (int r = 0; r < RG; ++r) {
-                        const unsigned char* vp = vg + size_t(q * RG + r) * KU * sizeof(TAB);
-                        if constexpr (sizeof(TAB) == 4 && KU == 4) {
-                            const float4 t = *reinterpret_cast<const float4*>(vp);
-                            v[r][0] = t.x; v[r][1] = t.y; v[r][2] = t.z; v[r][3] = t.w;
-                        } else if constexpr (sizeof(TAB) == 4) {
-                            const float2 t = *reinterpret_cast<const float2*>(vp);
-                            v[r][0] = t.x; v[r][1] = t.y;
-                        } else if constexpr (KU == 4) {
-                            const uint2 t = *reinterpret_cast<const uint2*>(vp);
-                            v[r][0] = __uint_as_float(t.x << 16); v[r][1] = __uint_as_float(t.x & 0xffff0000u);
-                            v[r][2] = __uint_as_float(t.y << 16); v[r][3] = __uint_as_float(t.y & 0xffff0000u);
+                    for (int q = 0; q < SUB; ++q) {
+                        int offs[KU];
+                        if constexpr (KU == 4) {
+                            const int4 o = *reinterpret_cast<const int4*>(og + q * KU);
+                            offs[0] = o.x; offs[1] = o.y; offs[2] = o.z; offs[3] = o.w;
                         } else {
-                            const uint32_t t = *reinterpret_cast<const uint32_t*>(vp);
-                            v[r][0] = __uint_as_float(t << 16); v[r][1] = __uint_as_float(t & 0xffff0000u);
+                            const int2 o = *reinterpret_cast<const int2*>(og + q * KU);
+                            offs[0] = o.x; offs[1] = o.y;
                         }
-                    }
+                        float v[RG][KU];
 #pragma unroll
-                    for (int t = 0; t < KU; ++t) {
-                        const uint32_t ba = uint32_t(offs[t]) + lane_off;
+                        for (int r = 0; r < RG; ++r) {
+                            const unsigned char* vp = vg + size_t(q * RG + r) * KU * sizeof(TAB);
+                            if constexpr (sizeof(TAB) == 4 && KU == 4) {
+                                const float4 t = *reinterpret_cast<const float4*>(vp);
+                                v[r][0] = t.x; v[r][1] = t.y; v[r][2] = t.z; v[r][3] = t.w;
+                            } else if constexpr (sizeof(TAB) == 4) {
+                                const float2 t = *reinterpret_cast<const float2*>(vp);
+                                v[r][0] = t.x; v[r][1] = t.y;
+                            } else if constexpr (KU == 4) {
+                                const uint2 t = *reinterpret_cast<const uint2*>(vp);
+                                v[r][0] = __uint_as_float(t.x << 16); v[r][1] = __uint_as_float(t.x & 0xffff0000u);
+                                v[r][2] = __uint_as_float(t.y << 16); v[r][3] = __uint_as_float(t.y & 0xffff0000u);
+                            } else {
+                                const uint32_t t = *reinterpret_cast<const uint32_t*>(vp);
+                                v[r][0] = __uint_as_float(t << 16); v[r][1] = __uint_as_float(t & 0xffff0000u);
+                            }
+                        }
 #pragma unroll
-                        for (int j = 0; j < Cfg::kChunks; ++j) {
-                            float b[EV];
-                            unpack<EV>(lds128_addr(ba + uint32_t(j) * 512u), b);
+                        for (int t = 0; t < KU; ++t) {
+                            const uint32_t ba = uint32_t(offs[t]) + lane_off;
 #pragma unroll
-                            for (int r = 0; r < RG; ++r)
+                            for (int j = 0; j < Cfg::kChunks; ++j) {
+                                float b[EV];
+                                unpack<EV>(lds128_addr(ba + uint32_t(j) * 512u), b);
 #pragma unroll
-                                for (int e = 0; e < EV; e += 2) {
-                                    float2& c2 = *reinterpret_cast<float2*>(&acc[q][r][j * EV + e]);
-                                    c2 = __ffma2_rn(make_float2(v[r][t], v[r][t]), make_float2(b[e], b[e + 1]), c2);
-                                }
+                                for (int r = 0; r < RG; ++r)
+#pragma unroll
+                                    for (int e = 0; e < EV; e += 2) {
+                                        float2& c2 = *reinterpret_cast<float2*>(&acc[q][r][j * EV + e]);
+                                        c2 = __ffma2_rn(make_float2(v[r][t], v[r][t]), make_float2(b[e], b[e + 1]), c2);
+                                    }
+                            }
                         }
                     }
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[buf]);
         }
-    }
-    cp_async_wait<0>();
-
-    if (a.split == 1) {
-        if (!warp_active) return;
-        TC* C = static_cast<TC*>(a.C);
+        STEN_TSTAMP(3);
+        if (a.split == 1) {
+            if (!warp_active) return;
+            TC* C = static_cast<TC*>(a.C);
 #pragma unroll
-        for (int q = 0; q < SUB; ++q)
+            for (int q = 0; q < SUB; ++q)
 #pragma unroll
-            for (int r = 0; r < RG; ++r) {
-                const int64_t row = m0 + int64_t(sub0 + q) * RG + r;
-                if (row >= a.M) continue;
+                for (int r = 0; r < RG; ++r) {
+                    const int64_t row = m0 + int64_t(sub0 + q) * RG + r;
+                    if (row >= a.M) continue;
 #pragma unroll
-                for (int j = 0; j < Cfg::kChunks; ++j)
-                    store_out<TC>(C, a.ldc, row, n0 + int64_t(j) * 32 * EV + lane * EV, a.N, &acc[q][r][j * EV],
-                                  EV, a.c_vec);
-            }
-        return;
+                    for (int j = 0; j < Cfg::kChunks; ++j)
+                        store_out<TC>(C, a.ldc, row, n0 + int64_t(j) * 32 * EV + lane * EV, a.N, &acc[q][r][j * EV],
+                                      EV, a.c_vec);
+                }
+            return;
+        }
     }
     // split-K: park the partial tile [BM][BN] (fp32) after the header, reduce over the cluster
     __syncthreads();
     float* tile = reinterpret_cast<float*>(smem + L.hdr);
+    if (warp < CW) {
 #pragma unroll
-    for (int q = 0; q < SUB; ++q)
+        for (int q = 0; q < SUB; ++q)
 #pragma unroll
-        for (int r = 0; r < RG; ++r) {
-            const int row = (sub0 + q) * RG + r;
+            for (int r = 0; r < RG; ++r) {
+                const int row = (sub0 + q) * RG + r;
 #pragma unroll
-            for (int j = 0; j < Cfg::kChunks; ++j)
+                for (int j = 0; j < Cfg::kChunks; ++j)
 #pragma unroll
-                for (int e4 = 0; e4 < EV; e4 += 4) {
-                    const int col = j * 32 * EV + lane * EV + e4;
-                    *reinterpret_cast<float4*>(tile + size_t(row) * BN + col) =
-                        make_float4(acc[q][r][j * EV + e4], acc[q][r][j * EV + e4 + 1], acc[q][r][j * EV + e4 + 2],
-                                    acc[q][r][j * EV + e4 + 3]);
-                }
-        }
+                    for (int e4 = 0; e4 < EV; e4 += 4) {
+                        const int col = j * 32 * EV + lane * EV + e4;
+                        *reinterpret_cast<float4*>(tile + size_t(row) * BN + col) =
+                            make_float4(acc[q][r][j * EV + e4], acc[q][r][j * EV + e4 + 1],
+                                        acc[q][r][j * EV + e4 + 2], acc[q][r][j * EV + e4 + 3]);
+                    }
+            }
+    }
+    STEN_TSTAMP(4);
     cluster_reduce_store<TC, BM, BN, NT>(smem + L.hdr, a, m0, n0);
+    STEN_TSTAMP(5);
 }
 
 }  // namespace sten

@@ -6,6 +6,8 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "tma_host.h"
 #include "sparsify.cuh"
@@ -103,12 +105,13 @@ int simt_rows_per_warp(int g) {
     return 1;
 }
 
-// SIMT tile variants (plan.tile), every one with 64 fp32 accumulators per lane:
-//   1: 8 warps,  TN = 8, BM = 64,  BN = 256 (fp32) / 256 (bf16)  -- 2 CTAs / SM
-//   2: 16 warps, TN = 8, BM = 128, BN = 256                      -- 1 CTA / SM
-//   3: 16 warps, TN = 4, BM = 256, BN = 128 (fp32 only)          -- 1 CTA / SM
+// SIMT tile variants (plan.tile), every one with 64 fp32 accumulators per consumer lane
+// (warps = consumers + 1 producer):
+//   1: 8 warps,  TN = 8, BM = 56,  BN = 256 (fp32) / 256 (bf16)  -- 2 CTAs / SM
+//   2: 16 warps, TN = 8, BM = 120, BN = 256                      -- 1 CTA / SM
+//   3: 16 warps, TN = 4, BM = 240, BN = 128 (fp32 only)          -- 1 CTA / SM
 struct SimtTile { int warps, tn, bm; };
-constexpr SimtTile kSimtTiles[4] = {{0, 0, 0}, {8, 8, 64}, {16, 8, 128}, {16, 4, 256}};
+constexpr SimtTile kSimtTiles[4] = {{0, 0, 0}, {8, 8, 56}, {16, 8, 120}, {16, 4, 240}};
 constexpr int kMaxSplit = 8;              // portable thread-block cluster size
 
 inline bool simt_tile_ok(int tile, sten_dtype ab) {
@@ -116,9 +119,27 @@ inline bool simt_tile_ok(int tile, sten_dtype ab) {
     return !(tile == 3 && ab == STEN_BF16);
 }
 
-// m-blocks per slab for the SIMT kernel
-int simt_slab_blocks(sten_nmg f, sten_dtype ab) {
-    return simt_kbs(f.n, f.m, ab == STEN_F32 ? simt_target_rows<float>() : simt_target_rows<bf16_t>());
+// Shared-memory budget per CTA: tile 1 runs two CTAs per SM, tiles 2/3 one.
+constexpr size_t kSmemPerSM = 233472;                                    // 228 KB
+inline size_t simt_smem_budget(int tile) { return tile == 1 ? kSmemPerSM / 2 - 1024 : 232448; }
+
+// m-blocks per K-slab for the SIMT kernel: the largest multiple of 4/gcd(n,4) whose
+// STAGES-deep ring fits the CTA's shared-memory budget (B slab <= 256 rows, TMA box limit).
+int simt_slab_blocks(sten_nmg f, sten_dtype ab, int tile) {
+    const int q = 4 / gcd_int(f.n, 4);
+    const int rg = simt_rows_per_warp(f.g);
+    const int warps = kSimtTiles[tile].warps, bm = kSimtTiles[tile].bm;
+    const int esz = ab == STEN_F32 ? 4 : 2;
+    const int bn = 32 * kSimtTiles[tile].tn;
+    const int nsub = bm / rg;
+    (void)warps;
+    int best = q;
+    for (int kbs = q; kbs * f.m <= 256 && kbs * f.n <= 64; kbs += q) {
+        const SimtLayout L(bm, bn, nsub, esz, 3, kbs, f.n, f.m);
+        if (L.total > simt_smem_budget(tile)) break;
+        best = kbs;
+    }
+    return best;
 }
 
 template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS>
@@ -145,7 +166,7 @@ sten_status launch_simt_cfg(SpmmArgs a, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned((a.N + Cfg::kBN - 1) / Cfg::kBN), unsigned((a.M + Cfg::kBM - 1) / Cfg::kBM),
                        unsigned(a.split));
-    cfg.blockDim = dim3(Cfg::kThreads);
+    cfg.blockDim = dim3(Cfg::kThreads);                        // consumers + the producer warp
     cfg.dynamicSmemBytes = L.total;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -243,17 +264,33 @@ sten_status plan_auto(sten_nmg f, sten_dtype ab, int64_t M, int64_t K, int64_t N
         return STEN_OK;
     }
     p->algo = STEN_ALGO_SIMT;
-    // B-operand reuse: want BM * n/m >= 32 rows per staged B element (L2 traffic <= 1/8 B per FMA)
-    int tile = 1;
-    if (64.0 * d < 32.0) tile = 2;
-    if (128.0 * d < 32.0 && ab == STEN_F32) tile = 3;
-    p->tile = tile;
-    const int64_t bm = kSimtTiles[tile].bm, bn = 32 * kSimtTiles[tile].tn;
-    const int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
-    const int64_t slots = kNumSMs * (tile == 1 ? 2 : 1);
-    const double t_kb = double(bm * bn * f.n) / (128.0 / (tile == 1 ? 2 : 1));  // clk per m-block per CTA
-    const double red = double(bm * bn * 4) / 20.0;                          // DSMEM bytes / (B/clk)
-    p->split_k = choose_split(tiles, slots, KB, kMaxSplit, t_kb, red);
+    // Cost model (cycles) over tile x split, calibrated on B200 (tools/sweep.py):
+    //   per-CTA FMA rate: min(measured steady-state rate, L2 share / bytes per FMA)
+    //   CTA time = ceil(KB/S) m-blocks of work + fixed prologue/epilogue + DSMEM reduce (S > 1)
+    //   kernel   = waves * CTA time, waves = ceil(tiles * S / resident CTAs)
+    const double esz = ab == STEN_F32 ? 4.0 : 2.0;
+    const double base_rate[4] = {0.0, 32.0, 70.0, 56.0};            // FMA/clk per CTA at 2:4
+    const double l2_bytes_per_clk_sm = 34.0;                          // ~10 TB/s over 148 SMs
+    double best_t = 1e300;
+    int best_tile = 1, best_split = 1;
+    for (int tile = 1; tile <= 3; ++tile) {
+        if (!simt_tile_ok(tile, ab)) continue;
+        const double bm = kSimtTiles[tile].bm, bn = 32.0 * kSimtTiles[tile].tn;
+        const int per_sm = tile == 1 ? 2 : 1;
+        const double bytes_per_fma = esz / (bm * d) + esz / bn;
+        const double rate = std::min(base_rate[tile], l2_bytes_per_clk_sm / per_sm / bytes_per_fma);
+        const int64_t tiles = ((M + int64_t(bm) - 1) / int64_t(bm)) * ((N + int64_t(bn) - 1) / int64_t(bn));
+        const int64_t slots = int64_t(kNumSMs) * per_sm;
+        for (int S = 1; S <= kMaxSplit && S <= KB; ++S) {
+            const double waves = double((tiles * S + slots - 1) / slots);
+            const double work = double((KB + S - 1) / S) * bm * bn * f.n / rate;
+            const double red = S > 1 ? bm * bn * 4.0 / 15.0 : 0.0;
+            const double t = waves * (work + 4000.0 + red);
+            if (t < best_t * 0.98) { best_t = t; best_tile = tile; best_split = S; }
+        }
+    }
+    p->tile = best_tile;
+    p->split_k = best_split;
     return STEN_OK;
 }
 
@@ -306,7 +343,7 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
     if (plan.algo == STEN_ALGO_SIMT) {
         a.v_async = (a.Kp % 4 == 0) && ((reinterpret_cast<uintptr_t>(values) & (4 * sab - 1)) == 0);
         a.idx_bytes = (M / f.g) * a.KB * f.n;
-        a.kbs = simt_slab_blocks(f, ab_dt);
+        a.kbs = simt_slab_blocks(f, ab_dt, plan.tile);
         // split-K parts are whole slabs; S = ceil(KB / per-part)
         const int64_t slabs = (a.KB + a.kbs - 1) / a.kbs;
         const int64_t per = (slabs + plan.split_k - 1) / plan.split_k;
@@ -484,5 +521,12 @@ int32_t sten_spmm_launch_count(const sten_spmm_plan* plan) {
 }
 
 int32_t sten_version(void) { return 1; }
+
+#ifdef STEN_TIMING
+// debug builds only: copy the per-CTA phase timestamps of the last SpMM launches
+int sten_debug_timing(void* host_out, int max_ctas) {
+    return cudaMemcpyFromSymbol(host_out, g_sten_timing, size_t(max_ctas) * 8 * 8) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 }  // extern "C"

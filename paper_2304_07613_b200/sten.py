@@ -76,7 +76,8 @@ def load(build_if_missing: bool = True):
         if not os.path.exists(_build.LIB):
             raise RuntimeError("libsten.so is missing (run paper_2304_07613_b200/build.py); "
                                "there is no CPU fallback")
-        lib = ctypes.CDLL(_build.LIB)
+        # STEN_LIB_PATH: load an instrumented debug build instead (tools/phase_timing.py)
+        lib = ctypes.CDLL(os.environ.get("STEN_LIB_PATH", _build.LIB))
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res
