@@ -1,32 +1,40 @@
-"""Multi-GPU partition of the grouped n:m SpMM (SURVEY.md 8(e)).
+"""Multi-GPU partition of the grouped n:m SpMM (SURVEY.md 8(e), DESIGN.md section 8).
 
 One process per GPU (torchrun), torch.distributed over NCCL for the plumbing.
-Two partitions, both with no collective inside the product itself:
+Tokens are independent columns of B and C, so the product itself needs no
+collective:
 
 * token (column) sharding -- the sparse weight (values, idx) is replicated,
-  rank p owns the dense-operand columns [c0_p, c1_p) and computes C[:, c0_p:c1_p];
-  an all-gather of the C shards follows only when a consumer needs all of C;
+  rank p owns columns [c0_p, c1_p) of B and computes C[:, c0_p:c1_p]; an
+  all-gather of the C shards follows only when a consumer needs all of C;
 * row sharding -- rank p owns whole groups [p*G/P, (p+1)*G/P) of the weight,
-  B is replicated, and the all-gather runs along M (contiguous in C).
+  B is replicated, and the all-gather runs along M (contiguous rows of C).
 
 Every rank uses the plan of the GLOBAL problem (sten_spmm_plan_query on the
-full shape), so the per-column summation order is the same as on one GPU and
-the gathered result equals the single-GPU product bit for bit (pin P11).
+full shape), so the per-column summation order equals the single-GPU one and
+the gathered result is bit-identical to the unsharded product (pin P11).
 
-The all-gather is chunk-pipelined on a side stream: the local column range is
-cut into `chunks` pieces; after piece i is computed on the compute stream its
-gather is enqueued on the comm stream while piece i+1 computes.
+The token all-gather is chunk-pipelined: the local columns are cut into
+`chunks` pieces; after a piece is computed on the compute stream its gather is
+enqueued on a side stream while the next piece computes.
+
+The compute step is injectable (`compute=`) so the partition / gather logic is
+testable on CPU with the gloo backend (tests/test_parallel_gloo.py); on GPUs it
+is always the C-ABI SpMM.
 """
 from __future__ import annotations
+
+from typing import Callable
 
 import torch
 import torch.distributed as dist
 
-from . import sten
+ComputeFn = Callable[[torch.Tensor, torch.Tensor], torch.Tensor]   # (B_cols, out) -> out
 
 
 def shard_range(n_total: int, world: int, rank: int, align: int = 8) -> tuple[int, int]:
-    """Contiguous, `align`-multiple shard boundaries (the last shard takes the rest)."""
+    """Contiguous shard [c0, c1) of n_total columns; shard widths are `align`-multiples
+    (16-byte aligned rows for bf16/fp32) except possibly the last."""
     per = -(-n_total // world)
     per = -(-per // align) * align
     c0 = min(n_total, rank * per)
@@ -34,98 +42,130 @@ def shard_range(n_total: int, world: int, rank: int, align: int = 8) -> tuple[in
     return c0, c1
 
 
+def padded_shard_width(n_total: int, world: int, align: int = 8) -> int:
+    per = -(-n_total // world)
+    return -(-per // align) * align
+
+
 def group_range(M: int, g: int, world: int, rank: int) -> tuple[int, int]:
+    """Rows [r0, r1) of whole groups owned by `rank` under row sharding."""
     G = M // g
     return (rank * G // world) * g, ((rank + 1) * G // world) * g
 
 
+def _world(group):
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
+
+
+def sten_compute(values, idx, n, m, g, plan, out_dtype) -> ComputeFn:
+    """The GPU compute step: C_cols = densify(values, idx) @ B_cols through the C ABI."""
+    from . import sten
+
+    def fn(B_cols: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        return sten.spmm_grouped_nm(values, idx, B_cols, n, m, g, out=out, plan=plan)
+    return fn
+
+
 class TokenShardedSpmm:
-    """C[:, shard] = densify(values, idx) @ B[:, shard] on every rank (+ optional all-gather)."""
+    """C[:, shard] = W_sparse @ B[:, shard] on every rank, optional all-gather of C."""
 
-    def __init__(self, values, idx, n, m, g, K, N_global, out_dtype=None, chunks: int = 1, group=None):
-        self.values, self.idx = values, idx
-        self.n, self.m, self.g, self.K = n, m, g, K
-        self.M = values.shape[0]
-        self.N_global = N_global
-        self.out_dtype = out_dtype or values.dtype
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+    def __init__(self, M: int, N_global: int, out_dtype: torch.dtype, device, compute: ComputeFn,
+                 chunks: int = 1, group=None):
+        self.M, self.N_global = M, N_global
+        self.out_dtype, self.device = out_dtype, torch.device(device)
+        self.compute = compute
         self.group = group
-        self.plan = sten.spmm_plan(n, m, g, self.M, K, N_global, ab_dtype=values.dtype, c_dtype=self.out_dtype)
-        per = -(-N_global // self.world)
-        self.n_local = -(-per // 8) * 8
+        self.world, self.rank = _world(group)
+        self.n_local = padded_shard_width(N_global, self.world)
         self.chunks = max(1, chunks)
-        self.comm_stream = torch.cuda.Stream() if values.is_cuda else None
+        self.use_streams = self.device.type == "cuda"
+        self.comm_stream = torch.cuda.Stream(device=self.device) if self.use_streams else None
 
-    def local_range(self):
+    @classmethod
+    def from_sten(cls, values, idx, n, m, g, K, N_global, out_dtype=None, chunks=1, group=None):
+        from . import sten
+        out_dtype = out_dtype or values.dtype
+        plan = sten.spmm_plan(n, m, g, values.shape[0], K, N_global, ab_dtype=values.dtype, c_dtype=out_dtype)
+        return cls(values.shape[0], N_global, out_dtype, values.device,
+                   sten_compute(values, idx, n, m, g, plan, out_dtype), chunks, group)
+
+    def local_range(self) -> tuple[int, int]:
         return shard_range(self.N_global, self.world, self.rank)
 
-    def forward_local(self, B_local: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        return sten.spmm_grouped_nm(self.values, self.idx, B_local, self.n, self.m, self.g, out=out,
-                                    out_dtype=self.out_dtype, plan=self.plan)
+    def forward_local(self, B_local: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((self.M, B_local.shape[1]), dtype=self.out_dtype, device=self.device)
+        return self.compute(B_local, out)
 
-    def forward_allgather(self, B_local: torch.Tensor, gathered: torch.Tensor | None = None) -> torch.Tensor:
-        """Compute the local shard chunk by chunk and all-gather each chunk as soon as
-        it is done.  Returns [world][M][n_local]; column j of rank p is global column
-        p*n_local + j (use `assemble` for a [M][N] view/copy)."""
-        M, nl = self.M, self.n_local
-        if gathered is None:
-            gathered = torch.empty((self.world, M, nl), dtype=self.out_dtype, device=B_local.device)
-        n_have = B_local.shape[1]
-        local = torch.zeros((M, nl), dtype=self.out_dtype, device=B_local.device)
-        step = -(-nl // self.chunks)
+    def _chunk_bounds(self):
+        step = -(-self.n_local // self.chunks)
         step = -(-step // 8) * 8
-        compute = torch.cuda.current_stream()
-        # gather chunk-wise into [world][chunk][M][step] staging, then scatter to layout
-        bounds = [(c, min(nl, c + step)) for c in range(0, nl, step)]
-        stage = [torch.empty((self.world, M, c1 - c0), dtype=self.out_dtype, device=B_local.device)
-                 for (c0, c1) in bounds]
-        for (c0, c1), st in zip(bounds, stage):
-            hi = min(c1, n_have)
-            piece = torch.empty((M, c1 - c0), dtype=self.out_dtype, device=B_local.device)
-            if hi > c0:
-                sten.spmm_grouped_nm(self.values, self.idx, B_local[:, c0:hi], self.n, self.m, self.g,
-                                     out=piece[:, : hi - c0], plan=self.plan)
-            if hi < c1:
-                piece[:, max(0, hi - c0):].zero_()
-            ev = torch.cuda.Event()
-            ev.record(compute)
-            with torch.cuda.stream(self.comm_stream):
-                self.comm_stream.wait_event(ev)
-                dist.all_gather_into_tensor(st, piece, group=self.group)
-                piece.record_stream(self.comm_stream)
-        compute.wait_stream(self.comm_stream)
-        for (c0, c1), st in zip(bounds, stage):
-            gathered[:, :, c0:c1].copy_(st)
-        del local
-        return gathered
+        return [(c, min(self.n_local, c + step)) for c in range(0, self.n_local, step)]
 
-    def assemble(self, gathered: torch.Tensor) -> torch.Tensor:
-        """[world][M][n_local] -> [M][N_global] (copy)."""
-        full = gathered.permute(1, 0, 2).reshape(self.M, self.world * self.n_local)
-        return full[:, : self.N_global].contiguous()
+    def forward_allgather(self, B_local: torch.Tensor) -> torch.Tensor:
+        """Compute the local shard chunk by chunk and all-gather every chunk as soon as it
+        is done (side stream on GPUs).  Returns C [M][N_global]."""
+        M, nl, world = self.M, self.n_local, self.world
+        have = B_local.shape[1]
+        bounds = self._chunk_bounds()
+        staged = []
+        compute_stream = torch.cuda.current_stream(self.device) if self.use_streams else None
+        for (c0, c1) in bounds:
+            piece = torch.zeros((M, c1 - c0), dtype=self.out_dtype, device=self.device)
+            hi = min(c1, have)
+            if hi > c0:
+                self.compute(B_local[:, c0:hi], piece[:, : hi - c0])
+            gathered = torch.empty((world * M, c1 - c0), dtype=self.out_dtype, device=self.device)
+            if self.use_streams:
+                ev = torch.cuda.Event()
+                ev.record(compute_stream)
+                with torch.cuda.stream(self.comm_stream):
+                    self.comm_stream.wait_event(ev)
+                    dist.all_gather_into_tensor(gathered, piece, group=self.group)
+                    piece.record_stream(self.comm_stream)
+                    gathered.record_stream(self.comm_stream)
+            elif world > 1:
+                parts = list(gathered.chunk(world, dim=0))
+                dist.all_gather(parts, piece, group=self.group)
+            else:
+                gathered.copy_(piece)
+            staged.append(gathered)
+        if self.use_streams:
+            compute_stream.wait_stream(self.comm_stream)
+        # assemble: rank p's local column j is global column p * n_local + j
+        full = torch.empty((M, world * nl), dtype=self.out_dtype, device=self.device)
+        for (c0, c1), gathered in zip(bounds, staged):
+            for p in range(world):
+                full[:, p * nl + c0: p * nl + c1] = gathered[p * M:(p + 1) * M]
+        return full[:, : self.N_global]
 
 
 class RowShardedSpmm:
-    """Rank p owns groups [p*G/P, (p+1)*G/P): C[rows_p, :] = W_p x B, then all-gather along M."""
+    """Rank p owns groups [p*G/P, (p+1)*G/P): C[rows_p, :] = W_p @ B, then all-gather along M."""
 
-    def __init__(self, values_local, idx_local, n, m, g, K, M_global, N, out_dtype=None, group=None):
-        self.values, self.idx = values_local, idx_local
-        self.n, self.m, self.g, self.K = n, m, g, K
-        self.M_global, self.N = M_global, N
-        self.out_dtype = out_dtype or values_local.dtype
+    def __init__(self, M_global: int, g: int, N: int, out_dtype: torch.dtype, device, compute: ComputeFn,
+                 group=None):
+        self.M_global, self.g, self.N = M_global, g, N
+        self.out_dtype, self.device = out_dtype, torch.device(device)
+        self.compute = compute
         self.group = group
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        # plan of the global shape: same per-column K order on every rank
-        self.plan = sten.spmm_plan(n, m, g, M_global, K, N, ab_dtype=values_local.dtype, c_dtype=self.out_dtype)
-
-    def forward_local(self, B: torch.Tensor, out=None) -> torch.Tensor:
-        return sten.spmm_grouped_nm(self.values, self.idx, B, self.n, self.m, self.g, out=out,
-                                    out_dtype=self.out_dtype, plan=self.plan)
+        self.world, self.rank = _world(group)
+        self.r0, self.r1 = group_range(M_global, g, self.world, self.rank)
 
     def forward_allgather(self, B: torch.Tensor) -> torch.Tensor:
-        local = self.forward_local(B)
-        rows = local.shape[0]
-        full = torch.empty((rows * self.world, self.N), dtype=self.out_dtype, device=B.device)
-        dist.all_gather_into_tensor(full, local.contiguous(), group=self.group)
-        return full
+        rows = [group_range(self.M_global, self.g, self.world, p) for p in range(self.world)]
+        maxr = max(r1 - r0 for r0, r1 in rows)
+        local = torch.zeros((maxr, self.N), dtype=self.out_dtype, device=self.device)
+        nr = self.r1 - self.r0
+        if nr:
+            self.compute(B, local[:nr])
+        gathered = torch.empty((self.world * maxr, self.N), dtype=self.out_dtype, device=self.device)
+        if self.world > 1:
+            if self.device.type == "cuda":
+                dist.all_gather_into_tensor(gathered, local, group=self.group)
+            else:
+                dist.all_gather(list(gathered.chunk(self.world, dim=0)), local, group=self.group)
+        else:
+            gathered.copy_(local)
+        return torch.cat([gathered[p * maxr: p * maxr + (r1 - r0)] for p, (r0, r1) in enumerate(rows)], dim=0)
