@@ -67,6 +67,8 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--lanes", type=int, default=3,
+                   help="streams the independent cases of a step are spread over (inside the graph)")
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu legs)")
     p.add_argument("--out", default=None, help="also append the JSON line to this file")
     return p.parse_args()
@@ -210,15 +212,40 @@ def make_sets(cases, R, device, dtype):
     return sets, host
 
 
-def run_step(cases, data, ev_pairs=None, ext=None, stream=None):
+def assign_lanes(cases, lanes: int):
+    """Longest-processing-time assignment of the independent cases to `lanes` streams."""
+    order = sorted(range(len(cases)), key=lambda k: -nz_flops(cases[k]))
+    load = [0.0] * lanes
+    lane_of = [0] * len(cases)
+    for k in order:
+        j = min(range(lanes), key=lambda t: load[t])
+        lane_of[k] = j
+        load[j] += nz_flops(cases[k])
+    return lane_of
+
+
+def run_step(cases, data, ev_pairs=None, ext=None, stream=None, lane_streams=None, lane_of=None):
+    """One step: sparsify + SpMM of every case.  With lane streams, the cases (independent
+    linears) run on several streams forked from / joined to `stream`."""
+    import torch
     from paper_2304_07613_b200 import sten
+    if lane_streams:
+        fork = torch.cuda.Event()
+        fork.record(stream)
+        for ls in lane_streams:
+            ls.wait_event(fork)
     for k, (c, d) in enumerate(zip(cases, data)):
-        sten.sparsify_grouped_nm(d["W"], c.n, c.m, c.g, values=d["values"], idx=d["idx"])
-        if ev_pairs is not None:
-            ext.record(ev_pairs[k][0], stream)
-        sten.spmm_grouped_nm(d["values"], d["idx"], d["B"], c.n, c.m, c.g, out=d["C"], plan=d["plan"])
-        if ev_pairs is not None:
-            ext.record(ev_pairs[k][1], stream)
+        s = lane_streams[lane_of[k]] if lane_streams else stream
+        with torch.cuda.stream(s):
+            sten.sparsify_grouped_nm(d["W"], c.n, c.m, c.g, values=d["values"], idx=d["idx"])
+            if ev_pairs is not None:
+                ext.record(ev_pairs[k][0], s)
+            sten.spmm_grouped_nm(d["values"], d["idx"], d["B"], c.n, c.m, c.g, out=d["C"], plan=d["plan"])
+            if ev_pairs is not None:
+                ext.record(ev_pairs[k][1], s)
+    if lane_streams:
+        for ls in lane_streams:
+            stream.wait_stream(ls)
 
 
 def bench_sten(args, rank, world, local_rank):
@@ -256,21 +283,26 @@ def bench_sten(args, rank, world, local_rank):
                 a.record(stream)
                 b.record(stream)
     torch.cuda.synchronize()
-    graphs = []
     use_graph = not args.no_graph
-    if use_graph:
+    lanes = max(1, min(args.lanes, len(cases))) if use_graph else 1
+
+    def build_graphs(n_lanes):
+        lane_streams = [torch.cuda.Stream(device) for _ in range(n_lanes)] if n_lanes > 1 else None
+        lane_of = assign_lanes(cases, n_lanes)
+        gs = []
         for r in range(R):
             gph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gph, stream=stream):
                 ext.record(step_ev[r][0], stream)
-                run_step(cases, sets[r], ev[r], ext, stream)
+                run_step(cases, sets[r], ev[r], ext, stream, lane_streams, lane_of)
                 ext.record(step_ev[r][1], stream)
-            graphs.append(gph)
-    torch.cuda.synchronize()
+            gs.append(gph)
+        torch.cuda.synchronize()
+        return gs
 
-    def one(i):
+    def one(graphs, i):
         r = i % R
-        if use_graph:
+        if graphs is not None:
             graphs[r].replay()
         else:
             with torch.cuda.stream(stream):
@@ -283,38 +315,52 @@ def bench_sten(args, rank, world, local_rank):
                     ev[r][k][1].record(stream)
                 step_ev[r][1].record(stream)
 
-    for i in range(args.warmup):
-        one(i)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    sampler = ClockSampler(local_rank) if (rank == 0 and not args.profile) else None
-    if sampler:
-        sampler.start()
-        time.sleep(0.3)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    step_ms, spmm_ms = [], [[] for _ in cases]
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for i in range(args.steps):
-        one(i)
-        # read back the events of this set before it is replayed again
-        if (i + 1) % R == 0 or i == args.steps - 1:
-            torch.cuda.synchronize()
-            for j in range(i - (i % R), i + 1):
-                r = j % R
-                step_ms.append(step_ev[r][0].elapsed_time(step_ev[r][1]))
-                for k in range(len(cases)):
-                    spmm_ms[k].append(ev[r][k][0].elapsed_time(ev[r][k][1]))
-    t1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = sampler.stop() if sampler else None
-    loop_ms = t0.elapsed_time(t1)
+    def timed_loop(graphs, sample_clocks):
+        """W warm-up steps, then exactly K timed steps bracketed by barrier + synchronize."""
+        for i in range(args.warmup):
+            one(graphs, i)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        sampler = ClockSampler(local_rank) if (sample_clocks and rank == 0 and not args.profile) else None
+        if sampler:
+            sampler.start()
+            time.sleep(0.3)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        step_ms, spmm_ms = [], [[] for _ in cases]
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            one(graphs, i)
+            # read back the events of this set before it is replayed again
+            if (i + 1) % R == 0 or i == args.steps - 1:
+                torch.cuda.synchronize()
+                for j in range(i - (i % R), i + 1):
+                    r = j % R
+                    step_ms.append(step_ev[r][0].elapsed_time(step_ev[r][1]))
+                    for k in range(len(cases)):
+                        spmm_ms[k].append(ev[r][k][0].elapsed_time(ev[r][k][1]))
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks = sampler.stop() if sampler else None
+        return step_ms, spmm_ms, t0.elapsed_time(t1), clocks
+
+    # pass 1 (headline): the step with the independent cases spread over `lanes` streams
+    g_conc = build_graphs(lanes) if use_graph else None
+    step_ms, spmm_conc_ms, loop_ms, clocks = timed_loop(g_conc, True)
+    # pass 2 (per-kernel roofline): the same step on one stream, so SpMM launches do not overlap
+    if lanes > 1:
+        del g_conc
+        g_seq = build_graphs(1)
+        seq_step_ms, spmm_ms, _, _ = timed_loop(g_seq, False)
+        del g_seq
+    else:
+        seq_step_ms, spmm_ms = step_ms, spmm_conc_ms
     total_ms = float(sum(step_ms))
     # max over ranks
     tt = torch.tensor([total_ms], device=device, dtype=torch.float64)
@@ -325,7 +371,8 @@ def bench_sten(args, rank, world, local_rank):
     flops_step = sum(eff_flops(c) for c in cases)
     value = flops_step * world * args.steps / (total_ms * 1e-3) / 1e9
 
-    # dominant kernel: the SpMM (fp32 -> CUDA-core FFMA bound, bf16 -> tensor / HBM)
+    # dominant kernel: the SpMM (fp32 -> CUDA-core FFMA bound, bf16 -> tensor / HBM), timed per
+    # launch in the single-stream pass (pass 2) so that launches do not overlap
     spmm_total_ms = sum(sum(x) for x in spmm_ms)
     spmm_nz = sum(nz_flops(c) for c in cases) * args.steps
     spmm_bytes_tot = sum(spmm_bytes(c) for c in cases) * args.steps
@@ -368,10 +415,14 @@ def bench_sten(args, rank, world, local_rank):
                    "parallelism": "dp%d (token-sharded, weight replicated)" % world,
                    "l2": "rotating %d input sets, %.0f MB > 3x L2 (%.0f MB)" % (R, R * set_bytes / 2 ** 20,
                                                                             l2 / 2 ** 20),
-                   "cuda_graph": use_graph, "step": "sparsify (a1-a3) + SpMM (a5-a7) per case"},
+                   "cuda_graph": use_graph, "streams": lanes,
+                   "step": "sparsify (a1-a3) + SpMM (a5-a7) per case; independent cases spread over %d "
+                           "streams in one CUDA graph" % lanes},
         "roofline": roof,
         "spmm_only": {"value": round(sum(eff_flops(c) for c in cases) * args.steps / (spmm_total_ms * 1e-3) / 1e9, 2),
-                      "unit": UNIT, "share_of_step": round(spmm_total_ms / sum(step_ms), 4)},
+                      "unit": UNIT, "share_of_step": round(spmm_total_ms / sum(seq_step_ms), 4),
+                      "single_stream_ms_per_step": round(sum(seq_step_ms) / len(seq_step_ms), 5),
+                      "note": "per-launch SpMM times from a second timed pass of the same step on one stream"},
         "per_case": per_case,
         "gpu_launches": launches_per_step * args.steps,
         "loop_ms_device": round(loop_ms, 3),
