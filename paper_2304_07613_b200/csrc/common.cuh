@@ -52,6 +52,11 @@ STEN_DEVICE_INLINE void cp_async4(void* smem, const void* gmem, int src_bytes) {
 STEN_DEVICE_INLINE void cp_async_mbar_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+// same, but the barrier's pending count is raised at issue and lowered when the copies land
+// (net zero arrivals: the phase cannot complete before the copies)
+STEN_DEVICE_INLINE void cp_async_mbar_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 STEN_DEVICE_INLINE void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 STEN_DEVICE_INLINE void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }

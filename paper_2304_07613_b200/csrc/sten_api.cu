@@ -203,26 +203,6 @@ sten_status launch_simt(const SpmmArgs& a, int tile, cudaStream_t st) {
     }
 }
 
-// Ordered reduction of split-K partials (mma.sync path): C = ((p0 + p1) + p2) + ...
-template <typename TC>
-__global__ void __launch_bounds__(256)
-splitk_reduce_kernel(const float* __restrict__ parts, int split, int64_t M, int64_t N,
-                     TC* __restrict__ C, int64_t ldc) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= M * N) return;
-    const int64_t r = i / N, c = i - r * N;
-    float s = parts[i];
-    for (int p = 1; p < split; ++p) s = __fadd_rn(s, parts[int64_t(p) * M * N + i]);
-    C[r * ldc + c] = from_f32<TC>(s);
-}
-
-template <typename TC>
-sten_status launch_reduce(const float* parts, int split, int64_t M, int64_t N, void* C, int64_t ldc,
-                          cudaStream_t st) {
-    splitk_reduce_kernel<TC><<<grid1d(M * N), 256, 0, st>>>(parts, split, M, N, static_cast<TC*>(C), ldc);
-    return last_cuda();
-}
-
 template <typename TC>
 __global__ void zero_fill_kernel(TC* C, int64_t M, int64_t N, int64_t ldc) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -256,11 +236,11 @@ sten_status plan_auto(sten_nmg f, sten_dtype ab, int64_t M, int64_t K, int64_t N
     if (ab == STEN_BF16 && mma_supported(f.g)) {
         p->algo = STEN_ALGO_MMA_SYNC;
         p->tile = f.g % 16 == 0 ? 2 : 1;
-        const int64_t bm = 256, bn = 64;
+        const int64_t bm = 256, bn = 128;
         const int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
-        const double t_kb = double(bm * bn * f.n) / 512.0;      // clk per m-block per CTA (MMA-bound guess)
-        const double red = double(M) * N * 8.0 / (kNumSMs * 40.0);
-        p->split_k = choose_split(tiles, kNumSMs, KB, 16, t_kb, red);
+        const double t_kb = double(bm * bn * f.n) / 700.0;      // clk per m-block per CTA (~700 MAC/clk/SM)
+        const double red = double(bm * bn * 4) / 15.0;          // DSMEM reduce of the tile
+        p->split_k = choose_split(tiles, kNumSMs, KB, kMaxSplit, t_kb, red);
         return STEN_OK;
     }
     p->algo = STEN_ALGO_SIMT;
@@ -324,7 +304,7 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
         return STEN_ERR_UNSUPPORTED;
     if (plan.algo == STEN_ALGO_MMA_SYNC && !(plan.tile == 1 || (plan.tile == 2 && f.g % 16 == 0)))
         return STEN_ERR_UNSUPPORTED;
-    if (plan.split_k < 1 || plan.split_k > 64) return STEN_ERR_UNSUPPORTED;
+    if (plan.split_k < 1 || plan.split_k > kMaxSplit) return STEN_ERR_UNSUPPORTED;
     if (M == 0 || N == 0) return STEN_OK;
     if (K == 0) {
         if (c_dt == STEN_F32) zero_fill_kernel<float><<<grid1d(M * N), 256, 0, st>>>(static_cast<float*>(C), M, N, ldc);
@@ -356,24 +336,11 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
         return s;
     }
 
-    // mma.sync path: split-K partials through a stream-ordered workspace + ordered reduce
-    const int split = int(plan.split_k > a.KB ? a.KB : plan.split_k);
-    a.kb_per_split = (a.KB + split - 1) / split;
-    a.split = split;
-    float* parts = nullptr;
-    if (split > 1) {
-        if (cudaMallocAsync(reinterpret_cast<void**>(&parts), size_t(split) * M * N * 4, st) != cudaSuccess)
-            return STEN_ERR_CUDA;
-        a.C = parts;
-    }
-    s = c_dt == STEN_F32 ? launch_mma<float>(a, plan.tile, split, st) : launch_mma<bf16_t>(a, plan.tile, split, st);
-    if (split > 1) {
-        if (s == STEN_OK)
-            s = c_dt == STEN_F32 ? launch_reduce<float>(parts, split, M, N, C, ldc, st)
-                                 : launch_reduce<bf16_t>(parts, split, M, N, C, ldc, st);
-        cudaFreeAsync(parts, st);
-    }
-    return s;
+    // mma.sync path (split-K partials reduced over the cluster inside the kernel)
+    a.v_async = (a.Kp % 8 == 0) && aligned16(values);
+    a.idx_bytes = (M / f.g) * a.KB * f.n;
+    return c_dt == STEN_F32 ? launch_mma<float>(a, plan.tile, plan.split_k, st)
+                            : launch_mma<bf16_t>(a, plan.tile, plan.split_k, st);
 }
 
 }  // namespace
@@ -515,9 +482,8 @@ const char* sten_algo_name(int32_t algo) {
 }
 
 int32_t sten_spmm_launch_count(const sten_spmm_plan* plan) {
-    if (!plan) return 1;
-    // SIMT reduces split-K partials inside the kernel (cluster DSMEM); mma.sync adds a reduce launch
-    return (plan->algo == STEN_ALGO_MMA_SYNC && plan->split_k > 1) ? 2 : 1;
+    (void)plan;   // every algorithm reduces split-K partials inside its kernel (cluster DSMEM)
+    return 1;
 }
 
 int32_t sten_version(void) { return 1; }

@@ -277,3 +277,13 @@ def test_baseline_configs_sampled(cfg):
                                    nthreads=oracle.max_threads())
         assert float(np.max(np.abs(Cs - C_ref) / np.maximum(Bound, 1e-30))) <= TOL[case.dtype] * (
             1 if case.dtype == "f32" else 0.05), case.label()
+
+
+@pytest.mark.parametrize("g", [8, 16])
+@pytest.mark.parametrize("split", [1, 3])
+def test_spmm_mma_unaligned_values(g, split):
+    """1:10 with K' = 41 per row: values rows are not 16-byte aligned (synchronous staging)."""
+    plan = sten.make_plan(sten.ALGO_MMA_SYNC, split_k=split, tile=2 if g % 16 == 0 else 1)
+    C, C_ref, Bound = _spmm_case(M=16 * g, K=410, N=136, n=1, m=10, g=g, dtype="bf16", plan=plan,
+                                 out_dtype=torch.float32, seed=g + split)
+    assert rel_err(C, C_ref, Bound) <= 1e-5
