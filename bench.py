@@ -383,6 +383,7 @@ def bench_sten(args, rank, world, local_rank):
         achieved = spmm_nz / (spmm_total_ms * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
                 "frac": round(achieved / peak, 4), "traffic": peaks.get("traffic_spmm"),
+                "algorithmic_bytes_per_launch": round(sum(spmm_bytes(c) for c in cases) / len(cases), 1),
                 "peak_source": peaks["fp32_source"], "kernel": "spmm_simt_kernel (CUDA-core FFMA)"}
     else:
         t_roof = sum(max(nz_flops(c) / (peaks["bf16_tflops"] * 1e12), spmm_bytes(c) / (peaks["hbm_gbs"] * 1e9))
