@@ -13,6 +13,7 @@
 #include "sparsify.cuh"
 #include "spmm_simt.cuh"
 #include "spmm_mma.cuh"
+#include "spmm_tc.cuh"
 
 using namespace sten;
 
@@ -293,13 +294,24 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
         if (plan_in->algo != STEN_ALGO_AUTO && plan_in->algo != plan.algo) {
             plan.algo = plan_in->algo;
             plan.tile = plan.algo == STEN_ALGO_SIMT ? 1 : (f.g % 16 == 0 ? 2 : 1);
+            if (plan.algo == STEN_ALGO_TCGEN05) {
+                plan.tile = f.g % 64 == 0 ? 3 : f.g % 32 == 0 ? 2 : 1;
+                plan.split_k = 1;
+            }
         }
         if (plan_in->tile > 0) plan.tile = plan_in->tile;
         if (plan_in->split_k > 0) plan.split_k = plan_in->split_k;
     }
     if (plan.algo == STEN_ALGO_MMA_SYNC && (ab_dt != STEN_BF16 || !mma_supported(f.g)))
         return STEN_ERR_UNSUPPORTED;
-    if (plan.algo != STEN_ALGO_SIMT && plan.algo != STEN_ALGO_MMA_SYNC) return STEN_ERR_UNSUPPORTED;
+    if (plan.algo == STEN_ALGO_TCGEN05) {
+        // tile t -> RB = 8 << t rows per MMA (16/32/64), RB | g; one K partition (no split-K)
+        if (ab_dt != STEN_BF16 || !tc_supported(f.g) || plan.tile < 1 || plan.tile > 3 ||
+            f.g % (8 << plan.tile) != 0 || plan.split_k != 1)
+            return STEN_ERR_UNSUPPORTED;
+    }
+    if (plan.algo != STEN_ALGO_SIMT && plan.algo != STEN_ALGO_MMA_SYNC && plan.algo != STEN_ALGO_TCGEN05)
+        return STEN_ERR_UNSUPPORTED;
     if (plan.algo == STEN_ALGO_SIMT && (!simt_tile_ok(plan.tile, ab_dt) || plan.split_k > kMaxSplit))
         return STEN_ERR_UNSUPPORTED;
     if (plan.algo == STEN_ALGO_MMA_SYNC && !(plan.tile == 1 || (plan.tile == 2 && f.g % 16 == 0)))
@@ -336,6 +348,11 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
         return s;
     }
 
+    if (plan.algo == STEN_ALGO_TCGEN05) {
+        a.v_async = (a.Kp % 8 == 0) && aligned16(values);
+        a.idx_bytes = (M / f.g) * a.KB * f.n;
+        return c_dt == STEN_F32 ? launch_tc<float>(a, plan.tile, st) : launch_tc<bf16_t>(a, plan.tile, st);
+    }
     // mma.sync path (split-K partials reduced over the cluster inside the kernel)
     a.v_async = (a.Kp % 8 == 0) && aligned16(values);
     a.idx_bytes = (M / f.g) * a.KB * f.n;

@@ -287,3 +287,34 @@ def test_spmm_mma_unaligned_values(g, split):
     C, C_ref, Bound = _spmm_case(M=16 * g, K=410, N=136, n=1, m=10, g=g, dtype="bf16", plan=plan,
                                  out_dtype=torch.float32, seed=g + split)
     assert rel_err(C, C_ref, Bound) <= 1e-5
+
+
+# ----------------------------------------------------------------------------------------
+# K5 tcgen05 (A gathered into TMEM, accumulators in TMEM), 16 | g
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("g,tile", [(16, 1), (32, 2), (64, 3), (64, 1), (128, 3)])
+@pytest.mark.parametrize("n,m", [(2, 4), (1, 4), (1, 10), (3, 6)])
+def test_spmm_tcgen05(g, tile, n, m):
+    plan = sten.make_plan(sten.ALGO_TCGEN05, split_k=1, tile=tile)
+    # M and N ragged vs the 256 x 128 CTA tile, several K slabs
+    C, C_ref, Bound = _spmm_case(M=max(g, 320 // g * g), K=72 * m, N=200, n=n, m=m, g=g, dtype="bf16", plan=plan,
+                                 out_dtype=torch.float32, seed=g + n + m + tile)
+    assert rel_err(C, C_ref, Bound) <= 1e-5
+
+
+@pytest.mark.parametrize("out", ["f32", "bf16"])
+def test_spmm_tcgen05_integer_exact_and_bf16_out(out):
+    n, m, g = 2, 4, 16
+    M, K, N = 512, 256, 384
+    W = synthetic.integer_matrix(M, K, seed=11, dtype="bf16")
+    B = synthetic.integer_matrix(K, N, seed=12, dtype="bf16")
+    v_ref, i_ref = oracle.sparsify(W, n, m, g)
+    C_ref, Bound = oracle.spmm(v_ref, i_ref, B, n, m, g)
+    v, i = gpu_sparsify(W, n, m, g, "bf16")
+    od = torch.float32 if out == "f32" else torch.bfloat16
+    C = sten.spmm_grouped_nm(v, i, dev(B, "bf16"), n, m, g, plan=sten.make_plan(sten.ALGO_TCGEN05, 1, 1),
+                             out_dtype=od)
+    if out == "f32":
+        assert np.array_equal(C.cpu().numpy().astype(np.float64), C_ref)
+    else:
+        assert rel_err(C, C_ref, Bound) <= TOL["bf16"]
