@@ -26,7 +26,8 @@
 #pragma once
 #include "common.cuh"
 #include "spmm_simt.cuh"   // SpmmArgs, store_out
-#include "spmm_mma.cuh"    // ldsm_x4_trans, mma_swz
+#include "spmm_mma.cuh"    // ldsm_x4_trans
+#include "tma_host.h"
 
 namespace sten {
 
@@ -97,7 +98,7 @@ struct TcCfg {
     static constexpr int kNRB = kBM / RB;        // row blocks (one MMA N = RB each)
     static constexpr int kRowBytes = kBN * 2;
     static constexpr int kStages = 3;
-    static constexpr int kNA = 16;               // A buffers in TMEM (8 columns each)
+    static constexpr int kNA = 8;                // A units in TMEM: 4 k16 steps x 8 columns = 32 columns each
     static constexpr int kTeams = 3;
     static constexpr int kThreads = 512;
 };
@@ -110,10 +111,10 @@ struct TcLayout {
         ksp = kbs * n;                                      // multiple of 16
         iwords = ksp / 4 + 1;
         hdr = 1024;                                         // mbarriers, TMEM base, idx bases
-        b_stage = align128(size_t(bk) * bn * 2);
+        b_stage = (size_t(bk) * bn * 2 + 1023) & ~size_t(1023);   // 2 x [bk][64 tokens], SWIZZLE_128B
         v_stage = align128(size_t(bm) * ksp * 2);           // [ksp/16][bm/8][2][8][8] bf16
         i_stage = align128(size_t(nrb) * iwords * 4);
-        stage = b_stage + v_stage + i_stage;
+        stage = (b_stage + v_stage + i_stage + 1023) & ~size_t(1023);
         stages = hdr;
         total = hdr + size_t(nstages) * stage;
     }
@@ -121,7 +122,7 @@ struct TcLayout {
 
 template <typename TC, int RB>
 __global__ void __launch_bounds__(512, 1)
-spmm_tc_kernel(const SpmmArgs a) {
+spmm_tc_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmV) {
     using Cfg = TcCfg<RB>;
     constexpr int BM = Cfg::kBM, BN = Cfg::kBN, NRB = Cfg::kNRB, ST = Cfg::kStages, NA = Cfg::kNA;
     constexpr int ROWB = Cfg::kRowBytes;
@@ -145,6 +146,7 @@ spmm_tc_kernel(const SpmmArgs a) {
     const int64_t n0 = int64_t(blockIdx.x) * BN;
     const int64_t m0 = int64_t(blockIdx.y) * BM;
     const int64_t kb_begin = 0, kb_end = a.KB;
+    (void)CPR;
     const int nslabs = int((kb_end - kb_begin + kbs - 1) / kbs);
 
     auto sB = [&](int buf) { return smem + L.stages + size_t(buf) * L.stage; };
@@ -153,7 +155,7 @@ spmm_tc_kernel(const SpmmArgs a) {
 
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
-            mbar_init(&full[s], 32);
+            mbar_init(&full[s], 32);          // idx cp.async arrivals (one per producer lane) + TMA bytes
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < NA; ++b) {
@@ -178,42 +180,22 @@ spmm_tc_kernel(const SpmmArgs a) {
 
     if (warp == 0) {
         // ======================= producer =======================
-        const bf16_t* __restrict__ V = static_cast<const bf16_t*>(a.values);
-        const bf16_t* __restrict__ Bm = static_cast<const bf16_t*>(a.B);
+        // B slab: two TMA boxes [bk rows][64 tokens] with 128-byte swizzle (chunk c of row r at
+        // c ^ (r & 7)); values: one 5-D TMA box that lands in the canonical K-major layout
+        // [ksp/16][BM/8][2][8 rows][8 k]; idx words: cp.async (arrive.noinc, one per lane).
+        const uint32_t tx_bytes = uint32_t(L.bk) * ROWB + uint32_t(BM * ksp * 2);
         for (int s = 0; s < nslabs; ++s) {
             const int buf = s % ST;
             if (s >= ST) mbar_wait(&empty[buf], uint32_t(((s / ST) - 1) & 1));
             const int64_t kb0 = kb_begin + int64_t(s) * kbs;
             const int nkb = int(min64(kbs, kb_end - kb0));
-            const int rows = nkb * m, ks = nkb * n;
-            // dense B slab (swizzled 16-byte chunks; see K4)
-            for (int e = lane; e < rows * CPR; e += 32) {
-                const int kr = e / CPR, cc = e % CPR;
-                const int kbl = kr / m, j = kr - kbl * m;
-                const int64_t col = n0 + int64_t(cc) * 8;
-                const int bytes = int(max64(0, min64(8, a.N - col))) * 2;
-                cp_async16(sB(buf) + size_t(kr) * ROWB + ((cc ^ mma_swz(kbl, j, n)) * 16),
-                           bytes ? Bm + (kb0 * m + kr) * a.ldb + col : Bm, bytes);
+            const int ks = nkb * n;
+            if (lane == 0) {
+                mbar_expect_tx(&full[buf], tx_bytes);
+                tma_load_2d(sB(buf), &tmB, &full[buf], int(n0), int(kb0 * m));
+                tma_load_2d(sB(buf) + size_t(L.bk) * 128, &tmB, &full[buf], int(n0) + 64, int(kb0 * m));
+                tma_load_5d(sV(buf), &tmV, &full[buf], 0, 0, 0, int(m0 / 8), int(kb0 * n / 16));
             }
-            // values in the canonical K-major layout: chunk (row r, step kt, half h) of 8 values
-            // at ((kt * BM/8 + r/8) * 2 + h) * 128 + (r % 8) * 16
-            const int cpr = ksp / 8;                       // 8-value chunks per row
-            for (int e = lane; e < BM * cpr; e += 32) {
-                const int r = e / cpr, c = e - r * cpr;
-                const int kt = c >> 1, h = c & 1;
-                const int64_t row = m0 + r;
-                const int k0 = c * 8;
-                unsigned char* dst = sV(buf) + ((size_t(kt) * (BM / 8) + r / 8) * 2 + h) * 128 + (r % 8) * 16;
-                if (a.v_async) {
-                    const int bytes = row < a.M ? max(0, min(8, ks - k0)) * 2 : 0;
-                    cp_async16(dst, bytes ? V + row * a.Kp + kb0 * n + k0 : V, bytes);
-                } else {
-                    for (int q = 0; q < 8; ++q)
-                        reinterpret_cast<bf16_t*>(dst)[q] =
-                            (row < a.M && k0 + q < ks) ? V[row * a.Kp + kb0 * n + k0 + q] : bf16_t(0);
-                }
-            }
-            // idx words of every row block's group
             for (int e = lane; e < NRB * iwords; e += 32) {
                 const int rb = e / iwords, w = e - rb * iwords;
                 const int64_t gb = gbase[rb];
@@ -222,18 +204,15 @@ spmm_tc_kernel(const SpmmArgs a) {
                 const int bytes = gb >= 0 ? int(max64(0, min64(4, min64(a.idx_bytes, start + ks) - woff))) : 0;
                 cp_async4(sI(buf) + size_t(e) * 4, bytes ? a.idx + woff : a.idx, bytes);
             }
-            // the values are read by the tensor core (async proxy): wait for this lane's copies,
-            // make them visible to the async proxy, then arrive
-            cp_async_commit();
-            cp_async_wait<0>();
-            fence_proxy_async_smem();
-            mbar_arrive(&full[buf]);
+            cp_async_mbar_arrive_noinc(&full[buf]);
         }
     } else if (warp == 1) {
         // ======================= MMA issuer (one thread) =======================
+        // work unit u = (slab, row block): all k16 steps of the slab for that row block; its
+        // gathered A occupies TMEM columns [256 + 32 (u % NA), +8 * ksteps)
         if (lane == 0) {
             const uint32_t idesc = tc_idesc(RB);
-            int i = 0;
+            int u = 0;
             for (int s = 0; s < nslabs; ++s) {
                 const int buf = s % ST;
                 mbar_wait(&full[buf], uint32_t((s / ST) & 1));
@@ -242,17 +221,16 @@ spmm_tc_kernel(const SpmmArgs a) {
                 const int ks = int(min64(kbs, kb_end - kb0)) * n;
                 const int ksteps = (ks + 15) / 16;
                 const uint32_t vbase = smem_u32(sV(buf));
-                for (int kt = 0; kt < ksteps; ++kt) {
-                    for (int rb = 0; rb < NRB; ++rb, ++i) {
-                        const int ab = i % NA;
-                        mbar_wait(&aready[ab], uint32_t((i / NA) & 1));
-                        tc_fence_after();
+                for (int rb = 0; rb < NRB; ++rb, ++u) {
+                    const int ab = u % NA;
+                    mbar_wait(&aready[ab], uint32_t((u / NA) & 1));
+                    tc_fence_after();
+                    for (int kt = 0; kt < ksteps; ++kt) {
                         const uint32_t bsa = vbase + uint32_t(((kt * (BM / 8) + rb * (RB / 8)) * 2) * 128);
-                        const uint64_t bdesc = tc_sdesc(bsa, 128, 256);
-                        tc_mma_ts(tmem_d + uint32_t(rb * RB), tmem_a + uint32_t(ab * 8), bdesc, idesc,
-                                  (s > 0 || kt > 0) ? 1u : 0u);
-                        tc_commit(&afree[ab]);
+                        tc_mma_ts(tmem_d + uint32_t(rb * RB), tmem_a + uint32_t(ab * 32 + kt * 8), tc_sdesc(bsa, 128, 256),
+                                  idesc, (s > 0 || kt > 0) ? 1u : 0u);
                     }
+                    tc_commit(&afree[ab]);
                 }
                 (void)ksteps_full;
                 tc_commit(&empty[buf]);
@@ -267,48 +245,45 @@ spmm_tc_kernel(const SpmmArgs a) {
         const int mi = lane >> 3, rr = lane & 7;
         const int slot = (rr >> 1) * 4 + (mi & 1) * 2 + (rr & 1);     // k slot 0..15 this lane addresses
         const int tok8 = (mi >> 1);                                     // +8 tokens for matrices 2, 3
-        int i = 0;
+        int u = 0;
         for (int s = 0; s < nslabs; ++s) {
             const int buf = s % ST;
             const int64_t kb0 = kb_begin + int64_t(s) * kbs;
             const int ks = int(min64(kbs, kb_end - kb0)) * n;
             const int ksteps = (ks + 15) / 16;
             bool waited = false;
-            for (int kt = 0; kt < ksteps; ++kt) {
-                for (int rb = 0; rb < NRB; ++rb, ++i) {
-                    if (i % TEAMS != team) continue;
-                    if (!waited) {
-                        mbar_wait(&full[buf], uint32_t((s / ST) & 1));
-                        waited = true;
-                    }
-                    const int ab = i % NA;
-                    if (i >= NA) mbar_wait(&afree[ab], uint32_t(((i / NA) - 1) & 1));
-                    tc_fence_after();
-                    // staged row of the kept k this lane addresses
+            for (int rb = 0; rb < NRB; ++rb, ++u) {
+                if (u % TEAMS != team) continue;
+                if (!waited) {
+                    mbar_wait(&full[buf], uint32_t((s / ST) & 1));
+                    waited = true;
+                }
+                const int ab = u % NA;
+                if (u >= NA) mbar_wait(&afree[ab], uint32_t(((u / NA) - 1) & 1));
+                tc_fence_after();
+                const int64_t start = gbase[rb] + kb0 * n;
+                const uint8_t* ib = sI(buf) + size_t(rb) * iwords * 4 + int(start & 3);
+                for (int kt = 0; kt < ksteps; ++kt) {
+                    // staged row of the kept k this lane addresses (padded slots: row 0, values 0)
                     const int kk = kt * 16 + slot;
-                    int rowoff = 0, swz = 0;
-                    if (kk < ks) {
-                        const int64_t start = gbase[rb] + kb0 * n;
-                        const uint8_t* ib = sI(buf) + size_t(rb) * iwords * 4 + int(start & 3);
-                        const int kbl = kk / n, j = ib[kk];
-                        rowoff = (kbl * m + j) * ROWB;
-                        swz = mma_swz(kbl, j, n);
-                    }
-                    const uint32_t rowaddr = smem_u32(sB(buf)) + uint32_t(rowoff);
+                    const int kr = kk < ks ? (kk / n) * m + ib[kk] : 0;
+                    const uint32_t rowaddr = smem_u32(sB(buf)) + uint32_t(kr * 128);
+                    const int swz = kr & 7;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int tok = 32 * q + 16 * h;                   // first token of the 16
-                        const int chunk = tok / 8 + tok8;
+                        const int chunk = tok / 8 + tok8;                  // 16-byte token chunk 0..15
+                        const uint32_t half = uint32_t(chunk >> 3) * uint32_t(L.bk) * 128u;
                         uint32_t r0, r1, r2, r3;
-                        ldsm_x4_trans(rowaddr + uint32_t((chunk ^ swz) * 16), r0, r1, r2, r3);
+                        ldsm_x4_trans(rowaddr + half + uint32_t(((chunk & 7) ^ swz) * 16), r0, r1, r2, r3);
                         // 16x256b: (lane t/4, col 2(t%4)), (.., +1), (lane t/4+8, ..), (.., +1)
-                        tmem_st_16x256b(tmem_a + uint32_t(ab * 8) + (uint32_t(tok) << 16), r0, r1, r2, r3);
+                        tmem_st_16x256b(tmem_a + uint32_t(ab * 32 + kt * 8) + (uint32_t(tok) << 16), r0, r1, r2, r3);
                     }
-                    tmem_wait_st();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&aready[ab]);
                 }
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&aready[ab]);
             }
         }
     }
@@ -367,11 +342,31 @@ inline cudaError_t launch_tc_cfg(SpmmArgs a, cudaStream_t st) {
     a.kb_per_split = a.KB;
     const size_t smem = tc_smem<RB>(a.kbs, a.n, a.m);
     if (smem > 232448) return cudaErrorInvalidValue;
+    const TcLayout L(Cfg::kBM, Cfg::kBN, Cfg::kNRB, Cfg::kStages, a.kbs, a.n, a.m);
+    CUtensorMap tmB, tmV;
+    memset(&tmB, 0, sizeof(tmB));
+    memset(&tmV, 0, sizeof(tmV));
+    {   // B [K][ldb] bf16: box {64 tokens, bk rows}, 128-byte swizzle
+        const uint64_t dims[2] = {uint64_t(a.N), uint64_t(a.K)};
+        const uint64_t strides[1] = {uint64_t(a.ldb) * 2};
+        const uint32_t box[2] = {64u, uint32_t(L.bk)};
+        if (!make_tmap_nd(&tmB, a.B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dims, strides, box,
+                          CU_TENSOR_MAP_SWIZZLE_128B))
+            return cudaErrorInvalidValue;
+    }
+    {   // values [M][Kp] bf16 viewed as {8 k, 8 rows, 2 halves, M/8 row groups, Kp/16 steps}
+        const uint64_t dims[5] = {8, 8, 2, uint64_t((a.M + 7) / 8), uint64_t(a.Kp / 16)};
+        const uint64_t strides[4] = {uint64_t(a.Kp) * 2, 16, uint64_t(a.Kp) * 16, 32};
+        const uint32_t box[5] = {8, 8, 2, uint32_t(Cfg::kBM / 8), uint32_t(L.ksp / 16)};
+        if (!make_tmap_nd(&tmV, a.values, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, dims, strides, box,
+                          CU_TENSOR_MAP_SWIZZLE_NONE))
+            return cudaErrorInvalidValue;
+    }
     auto kern = spmm_tc_kernel<TC, RB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     dim3 grid(unsigned((a.N + Cfg::kBN - 1) / Cfg::kBN), unsigned((a.M + Cfg::kBM - 1) / Cfg::kBM));
-    kern<<<grid, Cfg::kThreads, smem, st>>>(a);
+    kern<<<grid, Cfg::kThreads, smem, st>>>(a, tmB, tmV);
     return cudaGetLastError();
 }
 

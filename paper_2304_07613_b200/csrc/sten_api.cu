@@ -349,7 +349,9 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
     }
 
     if (plan.algo == STEN_ALGO_TCGEN05) {
-        a.v_async = (a.Kp % 8 == 0) && aligned16(values);
+        // values are TMA-loaded as 16-k steps: K' % 16 == 0 and 16-byte aligned rows
+        if (a.Kp % 16 != 0 || !aligned16(values)) return STEN_ERR_UNSUPPORTED;
+        a.v_async = true;
         a.idx_bytes = (M / f.g) * a.KB * f.n;
         return c_dt == STEN_F32 ? launch_tc<float>(a, plan.tile, st) : launch_tc<bf16_t>(a, plan.tile, st);
     }

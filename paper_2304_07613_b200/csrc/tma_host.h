@@ -50,4 +50,17 @@ inline bool make_tmap_3d(CUtensorMap* map, const void* base, CUtensorMapDataType
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Generic rank-r tiled map (dims/strides/box innermost first; strides has r-1 entries, bytes).
+inline bool make_tmap_nd(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int rank, const uint64_t* dims,
+                         const uint64_t* strides, const uint32_t* box, CUtensorMapSwizzle swizzle) {
+    auto fn = tma_encode_fn();
+    if (!fn || rank < 1 || rank > 5) return false;
+    cuuint64_t d[5], st[4];
+    cuuint32_t b[5], e[5];
+    for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; e[i] = 1; }
+    for (int i = 0; i + 1 < rank; ++i) st[i] = strides[i];
+    return fn(map, dt, cuuint32_t(rank), const_cast<void*>(base), d, st, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace sten

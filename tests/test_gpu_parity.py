@@ -297,9 +297,18 @@ def test_spmm_mma_unaligned_values(g, split):
 def test_spmm_tcgen05(g, tile, n, m):
     plan = sten.make_plan(sten.ALGO_TCGEN05, split_k=1, tile=tile)
     # M and N ragged vs the 256 x 128 CTA tile, several K slabs
-    C, C_ref, Bound = _spmm_case(M=max(g, 320 // g * g), K=72 * m, N=200, n=n, m=m, g=g, dtype="bf16", plan=plan,
+    # K' = 64 n per row (the tcgen05 path stages values in 16-k steps); 64 m-blocks = several slabs
+    C, C_ref, Bound = _spmm_case(M=max(g, 320 // g * g), K=64 * m, N=200, n=n, m=m, g=g, dtype="bf16", plan=plan,
                                  out_dtype=torch.float32, seed=g + n + m + tile)
     assert rel_err(C, C_ref, Bound) <= 1e-5
+
+
+def test_spmm_tcgen05_rejects_unaligned_kept():
+    v = torch.zeros((32, 72), dtype=torch.bfloat16, device="cuda")      # K' = 72: not a multiple of 16
+    i = torch.zeros((2, 72, 1), dtype=torch.uint8, device="cuda")
+    B = torch.zeros((288, 64), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(sten.StenError):
+        sten.spmm_grouped_nm(v, i, B, 1, 4, 16, plan=sten.make_plan(sten.ALGO_TCGEN05, 1, 1))
 
 
 @pytest.mark.parametrize("out", ["f32", "bf16"])
