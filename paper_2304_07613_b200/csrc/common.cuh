@@ -101,12 +101,13 @@ STEN_DEVICE_INLINE void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 STEN_DEVICE_INLINE void mbar_wait(uint64_t* bar, uint32_t phase) {
+    // try_wait with a suspend-time hint: the waiting warp sleeps instead of spinning on issue slots
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
+        "r"(phase), "r"(0x989680)
         : "memory");
 }
 // 2-D tiled TMA load of box {x..x+bx, y..y+by} (x innermost) into shared memory;
@@ -127,6 +128,13 @@ STEN_DEVICE_INLINE void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* 
         : "memory");
 }
 
+STEN_DEVICE_INLINE void tma_load_4d(void* smem_dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+        "[%2];\n" ::"r"(smem_u32(smem_dst)),
+        "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
 STEN_DEVICE_INLINE void tma_load_5d(void* smem_dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2, int c3,
                                     int c4) {
     asm volatile(

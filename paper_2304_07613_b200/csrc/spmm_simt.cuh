@@ -44,8 +44,35 @@ __device__ unsigned long long g_sten_timing[16384][8];
             if (cta_ < 16384) g_sten_timing[cta_][i] = t_;                                               \
         }                                                                                                 \
     } while (0)
+// per-CTA accumulated cycles of named waits / phases (lane 0 of the warps that time them)
+__device__ unsigned long long g_sten_wait[16384][8];
+// per-slab event timeline of CTA 0 (slab < 256, event < 8): clock64 at the event
+__device__ long long g_sten_tl[256][8];
+#define STEN_TL(slab, ev)                                                                                 \
+    do {                                                                                                  \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && (slab) < 256)                \
+            g_sten_tl[(slab)][(ev)] = clock64();                                                          \
+    } while (0)
+__device__ long long g_sten_tl2[256][8];
+#define STEN_TL2(u, ev)                                                                                   \
+    do {                                                                                                  \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && (u) < 256)                   \
+            g_sten_tl2[(u)][(ev)] = clock64();                                                            \
+    } while (0)
+#define STEN_CLK(v) const long long v = clock64()
+#define STEN_WACC(i, t0_)                                                                                 \
+    do {                                                                                                  \
+        if ((threadIdx.x & 31) == 0) {                                                                    \
+            const unsigned cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);          \
+            if (cta_ < 16384) atomicAdd(&g_sten_wait[cta_][i], (unsigned long long)(clock64() - (t0_)));  \
+        }                                                                                                 \
+    } while (0)
 #else
 #define STEN_TSTAMP(i) do { } while (0)
+#define STEN_CLK(v) do { } while (0)
+#define STEN_TL(slab, ev) do { } while (0)
+#define STEN_TL2(u, ev) do { } while (0)
+#define STEN_WACC(i, t0_) do { } while (0)
 #endif
 
 // Arguments common to the SpMM kernels.
@@ -65,6 +92,7 @@ struct SpmmArgs {
     bool v_tma;            // values tile staged by a 3-D TMA box into [ksp/KU][BM][KU]
     bool v_async;          // else: values rows vector-aligned -> 16B (fp32) / 8B (bf16) cp.async
     int64_t idx_bytes;     // size of the idx array (bounds the aligned-down idx word loads)
+    int bperm;             // tcgen05 path: staged-row permutation of the B slab (tc_staged_row)
 };
 
 // WARPS = warps per CTA: WARPS-1 consumer warps + 1 producer warp.

@@ -234,6 +234,14 @@ sten_status plan_auto(sten_nmg f, sten_dtype ab, int64_t M, int64_t K, int64_t N
     memset(p, 0, sizeof(*p));
     const int64_t KB = K / f.m;
     const double d = double(f.n) / f.m;
+    if (ab == STEN_BF16 && tc_supported(f.g) && KB % 8 == 0 && K > 0 &&
+        ((M + 255) / 256) * ((N + 127) / 128) >= kNumSMs) {
+        // K5 tcgen05 (no split-K): needs at least one full wave of 256 x 128 tiles; largest RB | g
+        p->algo = STEN_ALGO_TCGEN05;
+        p->tile = f.g % 64 == 0 ? 3 : f.g % 32 == 0 ? 2 : 1;
+        p->split_k = 1;
+        return STEN_OK;
+    }
     if (ab == STEN_BF16 && mma_supported(f.g)) {
         p->algo = STEN_ALGO_MMA_SYNC;
         p->tile = f.g % 16 == 0 ? 2 : 1;
@@ -290,6 +298,12 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
     if ((reinterpret_cast<uintptr_t>(idx) & 3u) != 0) return STEN_ERR_UNSUPPORTED;
     sten_spmm_plan plan;
     plan_auto(f, ab_dt, M, K, N, c_dt, &plan);
+    if (plan.algo == STEN_ALGO_TCGEN05 && !aligned16(values) && (!plan_in || plan_in->algo == STEN_ALGO_AUTO)) {
+        // automatic choice only: tcgen05 TMA-loads the values, which needs a 16-byte aligned base
+        plan.algo = STEN_ALGO_MMA_SYNC;
+        plan.tile = f.g % 16 == 0 ? 2 : 1;
+        plan.split_k = 1;
+    }
     if (plan_in) {
         if (plan_in->algo != STEN_ALGO_AUTO && plan_in->algo != plan.algo) {
             plan.algo = plan_in->algo;
@@ -349,8 +363,9 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
     }
 
     if (plan.algo == STEN_ALGO_TCGEN05) {
-        // values are TMA-loaded as 16-k steps: K' % 16 == 0 and 16-byte aligned rows
-        if (a.Kp % 16 != 0 || !aligned16(values)) return STEN_ERR_UNSUPPORTED;
+        // B slabs are TMA-loaded in groups of 8 m-blocks (K % 8m == 0); values rows by TMA
+        // (16-byte aligned base; the row stride K' = n KB is then a multiple of 16 bytes)
+        if (a.KB % 8 != 0 || !aligned16(values)) return STEN_ERR_UNSUPPORTED;
         a.v_async = true;
         a.idx_bytes = (M / f.g) * a.KB * f.n;
         return c_dt == STEN_F32 ? launch_tc<float>(a, plan.tile, st) : launch_tc<bf16_t>(a, plan.tile, st);
@@ -511,6 +526,16 @@ int32_t sten_version(void) { return 1; }
 // debug builds only: copy the per-CTA phase timestamps of the last SpMM launches
 int sten_debug_timing(void* host_out, int max_ctas) {
     return cudaMemcpyFromSymbol(host_out, g_sten_timing, size_t(max_ctas) * 8 * 8) == cudaSuccess ? 0 : 1;
+}
+int sten_debug_timeline(void* host_out, int which) {
+    return cudaMemcpyFromSymbol(host_out, which ? g_sten_tl2 : g_sten_tl, sizeof(long long) * 256 * 8) == cudaSuccess ? 0 : 1;
+}
+int sten_debug_waits(void* host_out, int max_ctas, int reset) {
+    if (reset) {
+        static unsigned long long zeros[16384][8];
+        return cudaMemcpyToSymbol(g_sten_wait, zeros, sizeof(zeros)) == cudaSuccess ? 0 : 1;
+    }
+    return cudaMemcpyFromSymbol(host_out, g_sten_wait, size_t(max_ctas) * 8 * 8) == cudaSuccess ? 0 : 1;
 }
 #endif
 

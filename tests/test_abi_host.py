@@ -105,7 +105,13 @@ def test_empty_problems_are_noops():
 def test_plan_query():
     p = sten.spmm_plan(2, 4, 4, 768, 3072, 1024)
     assert p.algo == sten.ALGO_SIMT and 1 <= p.split_k <= 16 and p.tile >= 1
-    p = sten.spmm_plan(2, 4, 16, 1024, 4096, 16384, ab_dtype=__import__("torch").bfloat16)
+    bf16 = __import__("torch").bfloat16
+    # bf16, 16 | g, at least one full wave of 256 x 128 tiles: tcgen05 with the largest RB | g
+    p = sten.spmm_plan(2, 4, 16, 1024, 4096, 16384, ab_dtype=bf16)
+    assert p.algo == sten.ALGO_TCGEN05 and p.tile == 1 and p.split_k == 1
+    assert sten.spmm_plan(1, 4, 64, 1024, 4096, 16384, ab_dtype=bf16).tile == 3
+    # small grids keep the split-K mma.sync path
+    p = sten.spmm_plan(2, 4, 16, 768, 768, 1024, ab_dtype=bf16)
     assert p.algo == sten.ALGO_MMA_SYNC
     # the plan is a pure function of the shape
     assert sten.spmm_plan(1, 4, 4, 768, 768, 1024).as_dict() == sten.spmm_plan(1, 4, 4, 768, 768, 1024).as_dict()

@@ -303,10 +303,19 @@ def test_spmm_tcgen05(g, tile, n, m):
     assert rel_err(C, C_ref, Bound) <= 1e-5
 
 
-def test_spmm_tcgen05_rejects_unaligned_kept():
-    v = torch.zeros((32, 72), dtype=torch.bfloat16, device="cuda")      # K' = 72: not a multiple of 16
-    i = torch.zeros((2, 72, 1), dtype=torch.uint8, device="cuda")
-    B = torch.zeros((288, 64), dtype=torch.bfloat16, device="cuda")
+@pytest.mark.parametrize("n,m,kb", [(1, 4, 72), (2, 4, 72), (3, 6, 40)])
+def test_spmm_tcgen05_ragged_last_slab(n, m, kb):
+    """K' not a multiple of the 64-k slab (nor of 16): the last slab's k16 steps are part padding."""
+    plan = sten.make_plan(sten.ALGO_TCGEN05, split_k=1, tile=1)
+    C, C_ref, Bound = _spmm_case(M=272, K=kb * m, N=136, n=n, m=m, g=16, dtype="bf16", plan=plan,
+                                 out_dtype=torch.float32, seed=kb + n)
+    assert rel_err(C, C_ref, Bound) <= 1e-5
+
+
+def test_spmm_tcgen05_rejects_unaligned_blocks():
+    v = torch.zeros((32, 36), dtype=torch.bfloat16, device="cuda")      # K/m = 36 blocks: not a multiple of 8
+    i = torch.zeros((2, 36, 1), dtype=torch.uint8, device="cuda")
+    B = torch.zeros((144, 64), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(sten.StenError):
         sten.spmm_grouped_nm(v, i, B, 1, 4, 16, plan=sten.make_plan(sten.ALGO_TCGEN05, 1, 1))
 
