@@ -67,6 +67,7 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--no-tune", action="store_true", help="AUTO plans instead of sten_spmm_autotune")
     p.add_argument("--lanes", type=int, default=3,
                    help="streams the independent cases of a step are spread over (inside the graph)")
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu legs)")
@@ -269,6 +270,17 @@ def bench_sten(args, rank, world, local_rank):
     R = max(1, min(R, int(0.6 * free // max(1, set_bytes))))
     sets, host = make_sets(cases, R, device, dtype)
     stream = torch.cuda.Stream(device)
+    if not args.no_tune:
+        # measured plan choice per case (sten_spmm_autotune), outside the timed region
+        with torch.cuda.stream(stream):
+            for k, c in enumerate(cases):
+                d = sets[0][k]
+                sten.sparsify_grouped_nm(d["W"], c.n, c.m, c.g, values=d["values"], idx=d["idx"])
+                plan = sten.spmm_autotune(d["values"], d["idx"], d["B"], c.n, c.m, c.g, out=d["C"], reps=5,
+                                          stream=stream)
+                for r in range(R):
+                    sets[r][k]["plan"] = plan
+        torch.cuda.synchronize()
     ext = ExtEvents()
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in cases]
           for _ in range(R)]
@@ -417,6 +429,8 @@ def bench_sten(args, rank, world, local_rank):
                    "l2": "rotating %d input sets, %.0f MB > 3x L2 (%.0f MB)" % (R, R * set_bytes / 2 ** 20,
                                                                             l2 / 2 ** 20),
                    "cuda_graph": use_graph, "streams": lanes,
+                   "plans": "AUTO (cost model)" if args.no_tune else
+                            "sten_spmm_autotune per case (min of 5 timed launches per variant, before timing)",
                    "step": "sparsify (a1-a3) + SpMM (a5-a7) per case; independent cases spread over %d "
                            "streams in one CUDA graph" % lanes},
         "roofline": roof,
@@ -430,7 +444,47 @@ def bench_sten(args, rank, world, local_rank):
     }
     if clocks:
         out["clocks"] = clocks
+    if not args.profile:
+        out["context_dense"] = dense_context(cases, sets[0], dtype, device)
     return out, cases, host, dtype, g
+
+
+def dense_context(cases, data, dtype, device):
+    """SURVEY.md §8(d) on-box context: dense torch.matmul on densify(W) at the same shapes
+    (fp32 with TF32 disabled, or bf16), per case median of 10 launches with an L2 flush before
+    each; plus the sum as a step.  A reported baseline, not a target."""
+    import torch
+    from paper_2304_07613_b200 import sten
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=device)
+    per = []
+    try:
+        for c, d in zip(cases, data):
+            Wd = sten.densify(d["values"], d["idx"], c.n, c.m, c.g, c.Kp)
+            out = torch.empty((c.M, c.N), dtype=Wd.dtype, device=device)
+            torch.matmul(Wd, d["B"], out=out)
+            ts = []
+            for _ in range(10):
+                flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                torch.matmul(Wd, d["B"], out=out)
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ts.sort()
+            per.append(ts[len(ts) // 2])
+            del Wd, out
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    step_ms = sum(per)
+    return {"impl": "torch.matmul(densify(W), B) dense, %s%s" % (dtype, ", allow_tf32=False" if dtype == "f32" else ""),
+            "ms_per_step": round(step_ms, 5),
+            "value": round(sum(eff_flops(c) for c in cases) / (step_ms * 1e-3) / 1e9, 2), "unit": UNIT,
+            "per_case_us": [round(t * 1e3, 2) for t in per],
+            "note": "cuBLAS dense GEMM on the masked weight, one stream, cold L2; context, not a target"}
 
 
 def load_peaks():

@@ -128,6 +128,22 @@ sten_status sten_spmm_grouped_nm_ex(sten_nmg f, sten_dtype ab_dt,
                                     void* C, int64_t ldc, sten_dtype c_dt,
                                     const sten_spmm_plan* plan, void* stream);
 
+/* Measured plan choice for one SpMM shape (the on-device analogue of a GEMM
+ * library's heuristic + benchmark mode).  Runs every compiled variant that
+ * accepts the arguments -- SIMT tiles x split-K, and for bf16 the mma.sync
+ * tiles x split-K and the tcgen05 row blocks -- `reps` timed times each on
+ * `stream` (CUDA events; one untimed launch first) and writes the fastest
+ * (minimum time) to *best (the AUTO plan is always a candidate, so the result
+ * is never slower than AUTO on the measured launches).  Arguments are those of
+ * sten_spmm_grouped_nm_ex; C is scratch while tuning (its final contents are
+ * the product computed with the last candidate).  Synchronises `stream`.
+ * reps < 1 -> STEN_ERR_INVALID_ARG; argument errors as for the SpMM. */
+sten_status sten_spmm_autotune(sten_nmg f, sten_dtype ab_dt,
+                               const void* values, const uint8_t* idx, int64_t M, int64_t K,
+                               const void* B, int64_t ldb, int64_t N,
+                               void* C, int64_t ldc, sten_dtype c_dt,
+                               int32_t reps, void* stream, sten_spmm_plan* best);
+
 /* End-to-end sparse linear layer with HOST input/output buffers: copies
  * W_host [M][ldw] and B_host [K][ldb] to the device, sparsifies W, multiplies,
  * copies C back to C_host [M][ldc] and waits for the stream.  Host buffers

@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 #include "tma_host.h"
@@ -518,6 +519,69 @@ const char* sten_algo_name(int32_t algo) {
 int32_t sten_spmm_launch_count(const sten_spmm_plan* plan) {
     (void)plan;   // every algorithm reduces split-K partials inside its kernel (cluster DSMEM)
     return 1;
+}
+
+sten_status sten_spmm_autotune(sten_nmg f, sten_dtype ab_dt, const void* values, const uint8_t* idx, int64_t M,
+                               int64_t K, const void* B, int64_t ldb, int64_t N, void* C, int64_t ldc,
+                               sten_dtype c_dt, int32_t reps, void* stream, sten_spmm_plan* best) {
+    if (!best || reps < 1) return STEN_ERR_INVALID_ARG;
+    cudaStream_t st = as_stream(stream);
+    sten_spmm_plan auto_plan;
+    sten_status s = check_format(f);
+    if (s) return s;
+    if (!dtype_ok(ab_dt) || !dtype_ok(c_dt)) return STEN_ERR_INVALID_ARG;
+    if ((s = check_shape(f, M, K))) return s;
+    plan_auto(f, ab_dt, M, K, N, c_dt, &auto_plan);
+    // the AUTO call itself validates every argument; an error here is the caller's
+    if ((s = spmm_impl(f, ab_dt, values, idx, M, K, B, ldb, N, C, ldc, c_dt, nullptr, st))) return s;
+    std::vector<sten_spmm_plan> cand;
+    auto add = [&](int algo, int tile, int split) {
+        sten_spmm_plan p;
+        memset(&p, 0, sizeof(p));
+        p.algo = algo; p.tile = tile; p.split_k = split;
+        cand.push_back(p);
+    };
+    add(STEN_ALGO_AUTO, 0, 0);
+    for (int tile = 1; tile <= 3; ++tile)
+        for (int split = 1; split <= kMaxSplit; ++split) add(STEN_ALGO_SIMT, tile, split);
+    if (ab_dt == STEN_BF16) {
+        for (int tile = 1; tile <= 2; ++tile)
+            for (int split = 1; split <= kMaxSplit; ++split) add(STEN_ALGO_MMA_SYNC, tile, split);
+        for (int tile = 1; tile <= 3; ++tile) add(STEN_ALGO_TCGEN05, tile, 1);
+    }
+    cudaEvent_t e0, e1;
+    if (cudaEventCreate(&e0) != cudaSuccess) return STEN_ERR_CUDA;
+    if (cudaEventCreate(&e1) != cudaSuccess) { cudaEventDestroy(e0); return STEN_ERR_CUDA; }
+    float best_ms = 3.0e38f;
+    sten_spmm_plan best_plan = auto_plan;
+    sten_status rc = STEN_OK;
+    for (const sten_spmm_plan& p : cand) {
+        const sten_spmm_plan* pp = p.algo == STEN_ALGO_AUTO ? nullptr : &p;
+        if (spmm_impl(f, ab_dt, values, idx, M, K, B, ldb, N, C, ldc, c_dt, pp, st) != STEN_OK) {
+            cudaGetLastError();     // an unsupported variant: skip it
+            continue;
+        }
+        float t_min = 3.0e38f;
+        for (int r = 0; r < reps; ++r) {
+            cudaEventRecord(e0, st);
+            spmm_impl(f, ab_dt, values, idx, M, K, B, ldb, N, C, ldc, c_dt, pp, st);
+            cudaEventRecord(e1, st);
+            if (cudaEventSynchronize(e1) != cudaSuccess) { rc = STEN_ERR_CUDA; break; }
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            t_min = std::min(t_min, ms);
+        }
+        if (rc) break;
+        if (t_min < best_ms) {
+            best_ms = t_min;
+            best_plan = p.algo == STEN_ALGO_AUTO ? auto_plan : p;
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc) return rc;
+    *best = best_plan;
+    return STEN_OK;
 }
 
 int32_t sten_version(void) { return 1; }

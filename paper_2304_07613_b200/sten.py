@@ -52,6 +52,9 @@ SIGNATURES = {
                                             ctypes.POINTER(sten_spmm_plan)]),
     "sten_spmm_grouped_nm_ex": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64, _i64,
                                                _vp, _i64, ctypes.c_int, ctypes.POINTER(sten_spmm_plan), _vp]),
+    "sten_spmm_autotune": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64, _i64,
+                                          _vp, _i64, ctypes.c_int, ctypes.c_int32, _vp,
+                                          ctypes.POINTER(sten_spmm_plan)]),
     "sten_sparse_linear_host_workspace_size": (ctypes.c_int64, [sten_nmg, ctypes.c_int, _i64, _i64, _i64,
                                                                 ctypes.c_int]),
     "sten_sparse_linear_host": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _i64, _i64,
@@ -184,6 +187,20 @@ def spmm_grouped_nm(values: torch.Tensor, idx: torch.Tensor, B: torch.Tensor, n:
     else:
         _check(lib.sten_spmm_grouped_nm_ex(*args, ctypes.byref(plan), _stream(stream)), "sten_spmm_grouped_nm_ex")
     return out
+
+
+def spmm_autotune(values: torch.Tensor, idx: torch.Tensor, B: torch.Tensor, n: int, m: int, g: int,
+                  out: torch.Tensor, reps: int = 5, stream=None) -> sten_spmm_plan:
+    """Fastest compiled plan for this shape, measured on the device (out is scratch)."""
+    _cuda(values, "values")
+    _cuda(B, "B")
+    M = values.shape[0]
+    K, N = B.shape
+    plan = sten_spmm_plan()
+    _check(load().sten_spmm_autotune(sten_nmg(n, m, g), _dt(B), values.data_ptr(), idx.data_ptr(), M, K,
+                                     B.data_ptr(), _ld(B), N, out.data_ptr(), _ld(out), _dt(out), int(reps),
+                                     _stream(stream), ctypes.byref(plan)), "sten_spmm_autotune")
+    return plan
 
 
 def sparse_linear_host(W_host: torch.Tensor, B_host: torch.Tensor, n: int, m: int, g: int,

@@ -336,3 +336,23 @@ def test_spmm_tcgen05_integer_exact_and_bf16_out(out):
         assert np.array_equal(C.cpu().numpy().astype(np.float64), C_ref)
     else:
         assert rel_err(C, C_ref, Bound) <= TOL["bf16"]
+
+
+# ----------------------------------------------------------------------------------------
+# measured plan choice: the tuned plan is a valid plan and reproduces the oracle
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype,g", [("f32", 4), ("bf16", 16)])
+def test_spmm_autotune(dtype, g):
+    n, m = 2, 4
+    M, K, N = 16 * g, 512, 384
+    W = synthetic.weights(M, K, seed=31, dtype=dtype)
+    B = synthetic.activations(K, N, seed=31, dtype=dtype)
+    v_ref, i_ref = oracle.sparsify(W, n, m, g)
+    C_ref, Bound = oracle.spmm(v_ref, i_ref, B, n, m, g)
+    v, i = gpu_sparsify(W, n, m, g, dtype)
+    Bd = dev(B, dtype)
+    scratch = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    plan = sten.spmm_autotune(v, i, Bd, n, m, g, out=scratch, reps=2)
+    assert plan.algo in (sten.ALGO_SIMT, sten.ALGO_MMA_SYNC, sten.ALGO_TCGEN05)
+    C = sten.spmm_grouped_nm(v, i, Bd, n, m, g, out_dtype=torch.float32, plan=plan)
+    assert rel_err(C, C_ref, Bound) <= 1e-5
