@@ -79,6 +79,12 @@ STEN_DEVICE_INLINE float4 lds128_addr(uint32_t addr) {
     return v;
 }
 
+STEN_DEVICE_INLINE uint32_t lds32_addr(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.b32 %0, [%1];\n" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 // ---- mbarrier + TMA (cp.async.bulk.tensor) helpers ---------------------------------------
 STEN_DEVICE_INLINE void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");

@@ -399,8 +399,8 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
         // ======================= consumer warps =======================
         const bool warp_active = (m0 + int64_t(sub0) * RG) < a.M;
         const uint32_t lane_off = uint32_t(lane) * 16u;
+        const uint32_t inv_n = (65536u + uint32_t(n) - 1) / uint32_t(n);   // kk / n = (kk inv_n) >> 16, kk < 64
         const uint32_t zero_row = smem_u32(smem + L.zero);
-        int* wo = reinterpret_cast<int*>(smem + L.offs) + sub0 * ksp;   // [ksp/KU][SUB][KU], warp-private
         for (int s = 0; s < nslabs; ++s) {
             const int buf = s % ST;
             mbar_wait(&full[buf], uint32_t((s / ST) & 1));
@@ -410,28 +410,34 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
                 const int ks = int(min64(kbs, kb_end - kb0)) * n;
                 const int nkg = (ks + KU - 1) / KU;
                 const uint32_t bbase = smem_u32(sB(buf));
+                // idx bytes of sub q in this slab begin at byte (gbase & 3) of its first word (the
+                // slab start advances by ksp, a multiple of 4, so the misalignment is fixed); the KU
+                // row addresses of a step are computed in registers: two broadcast word loads, a
+                // funnel shift, block b = kk / n by multiply-shift (kk < 64)
+                uint32_t iaddr[SUB];
+                int imis[SUB];
 #pragma unroll
                 for (int q = 0; q < SUB; ++q) {
-                    const int64_t start = gbase[sub0 + q] + kb0 * n;
-                    const uint8_t* ib = sI(buf) + size_t(sub0 + q) * iwords * 4 + int(start & 3);
-                    for (int kk = lane; kk < ksp; kk += 32)
-                        wo[((kk / KU) * SUB + q) * KU + kk % KU] =
-                            kk < ks ? int(bbase) + ((kk / n) * m + ib[kk]) * ROWB : int(zero_row);
+                    iaddr[q] = smem_u32(sI(buf)) + uint32_t((sub0 + q) * iwords * 4);
+                    imis[q] = int(gbase[sub0 + q] & 3);
                 }
-                __syncwarp();
                 const unsigned char* vbase = sV(buf) + size_t(sub0) * RG * KU * sizeof(TAB);
                 for (int kg = 0; kg < nkg; ++kg) {
                     const unsigned char* vg = vbase + size_t(kg) * BM * KU * sizeof(TAB);
-                    const int* og = wo + kg * SUB * KU;
 #pragma unroll
                     for (int q = 0; q < SUB; ++q) {
                         int offs[KU];
-                        if constexpr (KU == 4) {
-                            const int4 o = *reinterpret_cast<const int4*>(og + q * KU);
-                            offs[0] = o.x; offs[1] = o.y; offs[2] = o.z; offs[3] = o.w;
-                        } else {
-                            const int2 o = *reinterpret_cast<const int2*>(og + q * KU);
-                            offs[0] = o.x; offs[1] = o.y;
+                        {
+                            const int o = imis[q] + kg * KU;
+                            const uint32_t wa = iaddr[q] + uint32_t(o & ~3);
+                            const uint32_t x = __funnelshift_r(lds32_addr(wa), lds32_addr(wa + 4u), uint32_t(o & 3) * 8u);
+#pragma unroll
+                            for (int t = 0; t < KU; ++t) {
+                                const int kk = kg * KU + t;
+                                const int b = int((uint32_t(kk) * inv_n) >> 16);
+                                const int j = int((x >> (8 * t)) & 0xffu);
+                                offs[t] = kk < ks ? int(bbase) + (b * m + j) * ROWB : int(zero_row);
+                            }
                         }
                         float v[RG][KU];
 #pragma unroll

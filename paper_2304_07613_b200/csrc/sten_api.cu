@@ -112,18 +112,24 @@ int simt_rows_per_warp(int g) {
 //   1: 8 warps,  TN = 8, BM = 56,  BN = 256 (fp32) / 256 (bf16)  -- 2 CTAs / SM
 //   2: 16 warps, TN = 8, BM = 120, BN = 256                      -- 1 CTA / SM
 //   3: 16 warps, TN = 4, BM = 240, BN = 128 (fp32 only)          -- 1 CTA / SM
+// and two narrow tiles for small grids (more CTAs per output without split-K), fp32 only:
+//   4: 8 warps,  TN = 4, BM = 112, BN = 128 (64 accumulators)    -- 2 CTAs / SM
+//   5: 8 warps,  TN = 4, BM = 56,  BN = 128 (32 accumulators)    -- 2 CTAs / SM
 struct SimtTile { int warps, tn, bm; };
-constexpr SimtTile kSimtTiles[4] = {{0, 0, 0}, {8, 8, 56}, {16, 8, 120}, {16, 4, 240}};
+constexpr SimtTile kSimtTiles[6] = {{0, 0, 0}, {8, 8, 56}, {16, 8, 120}, {16, 4, 240}, {8, 4, 112}, {8, 4, 56}};
+constexpr int kSimtNumTiles = 5;
 constexpr int kMaxSplit = 8;              // portable thread-block cluster size
 
 inline bool simt_tile_ok(int tile, sten_dtype ab) {
-    if (tile < 1 || tile > 3) return false;
-    return !(tile == 3 && ab == STEN_BF16);
+    if (tile < 1 || tile > kSimtNumTiles) return false;
+    return !(tile >= 3 && ab == STEN_BF16);
 }
 
-// Shared-memory budget per CTA: tile 1 runs two CTAs per SM, tiles 2/3 one.
+// Shared-memory budget per CTA: tiles 1, 4, 5 run two CTAs per SM, tiles 2/3 one.
 constexpr size_t kSmemPerSM = 233472;                                    // 228 KB
-inline size_t simt_smem_budget(int tile) { return tile == 1 ? kSmemPerSM / 2 - 1024 : 232448; }
+inline size_t simt_smem_budget(int tile) {
+    return (tile == 1 || tile >= 4) ? kSmemPerSM / 2 - 1024 : 232448;
+}
 
 // m-blocks per K-slab for the SIMT kernel: the largest multiple of 4/gcd(n,4) whose
 // STAGES-deep ring fits the CTA's shared-memory budget (B slab <= 256 rows, TMA box limit).
@@ -190,6 +196,12 @@ sten_status launch_simt_rg(const SpmmArgs& a, int tile, cudaStream_t st) {
         case 2: return launch_simt_cfg<TAB, TC, RG, 8, SUB8, 16>(a, st);
         case 3:
             if constexpr (sizeof(TAB) == 4) return launch_simt_cfg<TAB, TC, RG, 4, 2 * SUB8, 16>(a, st);
+            else return STEN_ERR_UNSUPPORTED;
+        case 4:
+            if constexpr (sizeof(TAB) == 4) return launch_simt_cfg<TAB, TC, RG, 4, 2 * SUB8, 8>(a, st);
+            else return STEN_ERR_UNSUPPORTED;
+        case 5:
+            if constexpr (sizeof(TAB) == 4) return launch_simt_cfg<TAB, TC, RG, 4, SUB8, 8>(a, st);
             else return STEN_ERR_UNSUPPORTED;
     }
     return STEN_ERR_UNSUPPORTED;
@@ -542,7 +554,7 @@ sten_status sten_spmm_autotune(sten_nmg f, sten_dtype ab_dt, const void* values,
         cand.push_back(p);
     };
     add(STEN_ALGO_AUTO, 0, 0);
-    for (int tile = 1; tile <= 3; ++tile)
+    for (int tile = 1; tile <= kSimtNumTiles; ++tile)
         for (int split = 1; split <= kMaxSplit; ++split) add(STEN_ALGO_SIMT, tile, split);
     if (ab_dt == STEN_BF16) {
         for (int tile = 1; tile <= 2; ++tile)
