@@ -68,6 +68,8 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graph", action="store_true")
     p.add_argument("--no-tune", action="store_true", help="AUTO plans instead of sten_spmm_autotune")
+    p.add_argument("--plans-out", default=None, help="write the per-case plans used to this JSON file")
+    p.add_argument("--plans-in", default=None, help="use the per-case plans of this JSON file (no tuning)")
     p.add_argument("--lanes", type=int, default=3,
                    help="streams the independent cases of a step are spread over (inside the graph)")
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu legs)")
@@ -270,7 +272,16 @@ def bench_sten(args, rank, world, local_rank):
     R = max(1, min(R, int(0.6 * free // max(1, set_bytes))))
     sets, host = make_sets(cases, R, device, dtype)
     stream = torch.cuda.Stream(device)
-    if not args.no_tune:
+    if args.plans_in:
+        # plans recorded by an earlier run (--plans-out): same kernels, no tuning launches (profiling)
+        with open(args.plans_in) as f:
+            recorded = json.load(f)
+        for k, c in enumerate(cases):
+            pd = recorded[c.label()]
+            plan = sten.make_plan(pd["algo"], pd["split_k"], pd["tile"])
+            for r in range(R):
+                sets[r][k]["plan"] = plan
+    elif not args.no_tune:
         # measured plan choice per case (sten_spmm_autotune), outside the timed region
         with torch.cuda.stream(stream):
             for k, c in enumerate(cases):
@@ -281,6 +292,9 @@ def bench_sten(args, rank, world, local_rank):
                 for r in range(R):
                     sets[r][k]["plan"] = plan
         torch.cuda.synchronize()
+    if args.plans_out and rank == 0:
+        with open(args.plans_out, "w") as f:
+            json.dump({c.label(): sets[0][k]["plan"].as_dict() for k, c in enumerate(cases)}, f, indent=1)
     ext = ExtEvents()
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in cases]
           for _ in range(R)]
@@ -429,7 +443,8 @@ def bench_sten(args, rank, world, local_rank):
                    "l2": "rotating %d input sets, %.0f MB > 3x L2 (%.0f MB)" % (R, R * set_bytes / 2 ** 20,
                                                                             l2 / 2 ** 20),
                    "cuda_graph": use_graph, "streams": lanes,
-                   "plans": "AUTO (cost model)" if args.no_tune else
+                   "plans": ("recorded (%s)" % os.path.basename(args.plans_in)) if args.plans_in else
+                            "AUTO (cost model)" if args.no_tune else
                             "sten_spmm_autotune per case (min of 5 timed launches per variant, before timing)",
                    "step": "sparsify (a1-a3) + SpMM (a5-a7) per case; independent cases spread over %d "
                            "streams in one CUDA graph" % lanes},
@@ -587,12 +602,20 @@ def cpu_baseline(cases, host, budget_s=15.0):
     oracle.build()
     nt = cores()
     cols = calibrate_cols(cases, host, nt, budget_s)
-    t_full, t_spent, _, _ = oracle_step_time(cases, host, cols, nt)
+    # whole steps are repeated until ~budget_s of CPU work when one (sampled) step is cheaper
+    fulls, spent = [], 0.0
+    while True:
+        t_full, t_spent, _, _ = oracle_step_time(cases, host, cols, nt)
+        fulls.append(t_full)
+        spent += t_spent
+        if spent >= budget_s or len(fulls) >= 50:
+            break
+    t_full = statistics.median(fulls)
     val = sum(eff_flops(c) for c in cases) / t_full / 1e9
     return {"value": round(val, 4), "unit": UNIT, "cores": nt, "kind": "oracle",
-            "sample": "one step: oracle sparsify of every full W + oracle SpMM (fp64, %d threads) on the first %d "
-                      "token columns of each case, extrapolated linearly to all %d tokens; %.1f s of CPU work"
-                      % (nt, cols, cases[0].N, t_spent)}
+            "sample": "median of %d steps: oracle sparsify of every full W + oracle SpMM (fp64, %d threads) on the "
+                      "first %d token columns of each case (of %d, time extrapolated linearly); %.1f s of CPU work"
+                      % (len(fulls), nt, cols, cases[0].N, spent)}
 
 
 def bench_reference(args, rank, world):

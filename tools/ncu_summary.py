@@ -28,6 +28,15 @@ FULL_METRICS = [
     "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
     "smsp__inst_executed.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+    # tcgen05 evidence (K5): UTCHMMA ops, tensor sub-pipe, TMEM pipe, TMA bytes
+    "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.sum",
+    "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.per_cycle_elapsed",
+    "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg",
+    "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active",
+    "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum",
+    "l2__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
 ]
 
 
@@ -55,8 +64,8 @@ def launches(tag):
     return path, rows
 
 
-def full(tag):
-    rep = os.path.join(OUT, tag + "_full.ncu-rep")
+def full(tag, suffix="_full"):
+    rep = os.path.join(OUT, tag + suffix + ".ncu-rep")
     raw = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], text=True)
     rows = list(csv.reader(raw.splitlines()))
     hdr = rows[0]
@@ -98,6 +107,10 @@ def main():
                        "launches): compare shares, not absolute times")
     rep, f = full(a.tag)
     summary["dominant_launch_full_set"] = f
+    if os.path.exists(os.path.join(OUT, a.tag + "_tc_full.ncu-rep")):
+        _, ftc = full(a.tag, "_tc_full")
+        ftc["note"] = "C3 1024x4096x16384 1:4 g=64 bf16, tcgen05 kernel (K5), first launch"
+        summary["tcgen05_launch_full_set"] = ftc
     with open(os.path.join(PROF, "ncu_r%s_summary.json" % a.round), "w") as fh:
         json.dump(summary, fh, indent=1)
     spmm = [v for k, v in summary["launch_list"].items() if k.startswith("spmm")]
