@@ -279,6 +279,30 @@ def test_baseline_configs_sampled(cfg):
             1 if case.dtype == "f32" else 0.05), case.label()
 
 
+@pytest.mark.parametrize("cfg,dtype,g,shard", [(3, "f32", 4, 1), (3, "bf16", 16, 1), (4, "bf16", 64, 8),
+                                                 (4, "f32", 4, 8)])
+def test_baseline_configs_c4_c5_sampled(cfg, dtype, g, shard):
+    """C4 (BERT-base encoder linears, 32768 tokens) and C5 (8192x8192 1:8) at their full sizes,
+    or at the per-GPU token shard of an 8-GPU run (N / 8), in the AUTO launch configuration;
+    sampled columns against the oracle."""
+    rng = np.random.default_rng(cfg + shard)
+    for case in synthetic.config_cases(cfg, g=g, dtype=dtype):
+        N = case.N // shard
+        W = synthetic.weights(case.M, case.K, seed=1234 + cfg, dtype=dtype, k_pad=case.k_pad)
+        v_ref, i_ref = oracle.sparsify(W, case.n, case.m, case.g)
+        v, i = gpu_sparsify(W, case.n, case.m, case.g, dtype)
+        assert np.array_equal(host(i), i_ref)
+        cols = np.sort(rng.choice(N, size=16, replace=False))
+        B = synthetic.activations(case.K, N, seed=1234 + cfg, dtype=dtype, k_pad=case.k_pad)
+        Bd = dev(B, dtype)
+        C = sten.spmm_grouped_nm(v, i, Bd, case.n, case.m, case.g, out_dtype=torch.float32)
+        C_ref, Bound = oracle.spmm(v_ref, i_ref, np.ascontiguousarray(B[:, cols]), case.n, case.m, case.g,
+                                   nthreads=oracle.max_threads())
+        Cs = C.cpu().numpy()[:, cols].astype(np.float64)
+        assert float(np.max(np.abs(Cs - C_ref) / np.maximum(Bound, 1e-30))) <= 1e-5, case.label()
+        del C, Bd
+
+
 @pytest.mark.parametrize("g", [8, 16])
 @pytest.mark.parametrize("split", [1, 3])
 def test_spmm_mma_unaligned_values(g, split):
