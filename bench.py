@@ -49,7 +49,7 @@ CONFIG_NAMES = {
     1: "C2 BERT-base linears {768x768,768x3072,3072x768} x {2:4,1:4,1:10} x 1024 tokens",
     2: "C3 BERT-large linears {1024x4096,4096x1024} x {1:4,2:8} x 16384 tokens",
     3: "C4 BERT-base encoder-layer linears (QKV,O,FFN1,FFN2) 2:4 x 32768 tokens",
-    4: "C5 8192x8192 1:8 x 65536 tokens, column-sharded + NCCL all-gather",
+    4: "C5 8192x8192 1:8 x 65536 tokens (one GPU's product; the token-sharded all-gather is parallel.TokenShardedSpmm)",
 }
 FP32_LANES_PER_SM = 128        # B200 CUDA-core FP32 lanes per SM (guide unit counts)
 NUM_SMS = 148
