@@ -400,6 +400,12 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
         const bool warp_active = (m0 + int64_t(sub0) * RG) < a.M;
         const uint32_t lane_off = uint32_t(lane) * 16u;
         const uint32_t inv_n = (65536u + uint32_t(n) - 1) / uint32_t(n);   // kk / n = (kk inv_n) >> 16, kk < 64
+        // fast row addressing when n | KU: slot t of k-step kg lies in block kg KU/n + t/n
+        const bool n_divides_ku = KU % n == 0;
+        const int kstep_bytes = n_divides_ku ? (KU / n) * m * ROWB : 0;
+        int tb[KU];
+#pragma unroll
+        for (int t = 0; t < KU; ++t) tb[t] = n_divides_ku ? (t / n) * m * ROWB : 0;
         const uint32_t zero_row = smem_u32(smem + L.zero);
         for (int s = 0; s < nslabs; ++s) {
             const int buf = s % ST;
@@ -422,6 +428,7 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
                     imis[q] = int(gbase[sub0 + q] & 3);
                 }
                 const unsigned char* vbase = sV(buf) + size_t(sub0) * RG * KU * sizeof(TAB);
+                const bool fast = n_divides_ku && ks % KU == 0;
                 for (int kg = 0; kg < nkg; ++kg) {
                     const unsigned char* vg = vbase + size_t(kg) * BM * KU * sizeof(TAB);
 #pragma unroll
@@ -431,12 +438,20 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
                             const int o = imis[q] + kg * KU;
                             const uint32_t wa = iaddr[q] + uint32_t(o & ~3);
                             const uint32_t x = __funnelshift_r(lds32_addr(wa), lds32_addr(wa + 4u), uint32_t(o & 3) * 8u);
+                            if (fast) {
+                                // n | KU and a full slab: block of slot t = kg KU / n + t / n, no padding
+                                const int rowbase = int(bbase) + kg * kstep_bytes;
 #pragma unroll
-                            for (int t = 0; t < KU; ++t) {
-                                const int kk = kg * KU + t;
-                                const int b = int((uint32_t(kk) * inv_n) >> 16);
-                                const int j = int((x >> (8 * t)) & 0xffu);
-                                offs[t] = kk < ks ? int(bbase) + (b * m + j) * ROWB : int(zero_row);
+                                for (int t = 0; t < KU; ++t)
+                                    offs[t] = rowbase + tb[t] + int((x >> (8 * t)) & 0xffu) * ROWB;
+                            } else {
+#pragma unroll
+                                for (int t = 0; t < KU; ++t) {
+                                    const int kk = kg * KU + t;
+                                    const int b = int((uint32_t(kk) * inv_n) >> 16);
+                                    const int j = int((x >> (8 * t)) & 0xffu);
+                                    offs[t] = kk < ks ? int(bbase) + (b * m + j) * ROWB : int(zero_row);
+                                }
                             }
                         }
                         float v[RG][KU];
