@@ -106,6 +106,12 @@ def spmm_bytes(c, out_size=None) -> float:
     return c.M * c.kept * s + (c.M // c.g) * (c.Kp // c.m) * c.n + c.Kp * c.N * s + c.M * c.N * so
 
 
+def sparsify_bytes(c) -> float:
+    """HBM roofline bytes of one sparsify launch: read W, write values and idx."""
+    s = esize(c.dtype)
+    return c.M * c.Kp * s + c.M * c.kept * s + (c.M // c.g) * (c.Kp // c.m) * c.n
+
+
 def cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -240,6 +246,8 @@ def run_step(cases, data, ev_pairs=None, ext=None, stream=None, lane_streams=Non
     for k, (c, d) in enumerate(zip(cases, data)):
         s = lane_streams[lane_of[k]] if lane_streams else stream
         with torch.cuda.stream(s):
+            if ev_pairs is not None:
+                ext.record(ev_pairs[k][2], s)
             sten.sparsify_grouped_nm(d["W"], c.n, c.m, c.g, values=d["values"], idx=d["idx"])
             if ev_pairs is not None:
                 ext.record(ev_pairs[k][0], s)
@@ -296,8 +304,8 @@ def bench_sten(args, rank, world, local_rank):
         with open(args.plans_out, "w") as f:
             json.dump({c.label(): sets[0][k]["plan"].as_dict() for k, c in enumerate(cases)}, f, indent=1)
     ext = ExtEvents()
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in cases]
-          for _ in range(R)]
+    # per case: (after sparsify, after SpMM, before sparsify)
+    ev = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in cases] for _ in range(R)]
     step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(R)]
 
     # warm-up (also JIT-free: the library is precompiled) then capture one graph per set;
@@ -305,14 +313,16 @@ def bench_sten(args, rank, world, local_rank):
     with torch.cuda.stream(stream):
         for r in range(R):
             run_step(cases, sets[r])
-            for a, b in ev[r] + [step_ev[r]]:
-                a.record(stream)
-                b.record(stream)
+            for evs in ev[r] + [step_ev[r]]:
+                for e in evs:
+                    e.record(stream)
     torch.cuda.synchronize()
     use_graph = not args.no_graph
     lanes = max(1, min(args.lanes, len(cases))) if use_graph else 1
 
     def build_graphs(n_lanes):
+        # per-case event nodes only in the single-stream graph (the per-kernel pass); the
+        # headline multi-stream graph carries just the two step events
         lane_streams = [torch.cuda.Stream(device) for _ in range(n_lanes)] if n_lanes > 1 else None
         lane_of = assign_lanes(cases, n_lanes)
         gs = []
@@ -320,7 +330,7 @@ def bench_sten(args, rank, world, local_rank):
             gph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gph, stream=stream):
                 ext.record(step_ev[r][0], stream)
-                run_step(cases, sets[r], ev[r], ext, stream, lane_streams, lane_of)
+                run_step(cases, sets[r], ev[r] if n_lanes == 1 else None, ext, stream, lane_streams, lane_of)
                 ext.record(step_ev[r][1], stream)
             gs.append(gph)
         torch.cuda.synchronize()
@@ -334,6 +344,7 @@ def bench_sten(args, rank, world, local_rank):
             with torch.cuda.stream(stream):
                 step_ev[r][0].record(stream)
                 for k, (c, d) in enumerate(zip(cases, sets[r])):
+                    ev[r][k][2].record(stream)
                     sten.sparsify_grouped_nm(d["W"], c.n, c.m, c.g, values=d["values"], idx=d["idx"])
                     ev[r][k][0].record(stream)
                     sten.spmm_grouped_nm(d["values"], d["idx"], d["B"], c.n, c.m, c.g, out=d["C"],
@@ -341,7 +352,7 @@ def bench_sten(args, rank, world, local_rank):
                     ev[r][k][1].record(stream)
                 step_ev[r][1].record(stream)
 
-    def timed_loop(graphs, sample_clocks):
+    def timed_loop(graphs, sample_clocks, per_case=True):
         """W warm-up steps, then exactly K timed steps bracketed by barrier + synchronize."""
         for i in range(args.warmup):
             one(graphs, i)
@@ -355,7 +366,7 @@ def bench_sten(args, rank, world, local_rank):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        step_ms, spmm_ms = [], [[] for _ in cases]
+        step_ms, spmm_ms, spars_ms = [], [[] for _ in cases], [[] for _ in cases]
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
@@ -367,26 +378,27 @@ def bench_sten(args, rank, world, local_rank):
                 for j in range(i - (i % R), i + 1):
                     r = j % R
                     step_ms.append(step_ev[r][0].elapsed_time(step_ev[r][1]))
-                    for k in range(len(cases)):
+                    for k in (range(len(cases)) if per_case else ()):
                         spmm_ms[k].append(ev[r][k][0].elapsed_time(ev[r][k][1]))
+                        spars_ms[k].append(ev[r][k][2].elapsed_time(ev[r][k][0]))
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         clocks = sampler.stop() if sampler else None
-        return step_ms, spmm_ms, t0.elapsed_time(t1), clocks
+        return step_ms, (spmm_ms, spars_ms), t0.elapsed_time(t1), clocks
 
     # pass 1 (headline): the step with the independent cases spread over `lanes` streams
     g_conc = build_graphs(lanes) if use_graph else None
-    step_ms, spmm_conc_ms, loop_ms, clocks = timed_loop(g_conc, True)
+    step_ms, spmm_conc_ms, loop_ms, clocks = timed_loop(g_conc, True, per_case=lanes == 1)
     # pass 2 (per-kernel roofline): the same step on one stream, so SpMM launches do not overlap
     if lanes > 1:
         del g_conc
         g_seq = build_graphs(1)
-        seq_step_ms, spmm_ms, _, _ = timed_loop(g_seq, False)
+        seq_step_ms, (spmm_ms, spars_ms), _, _ = timed_loop(g_seq, False)
         del g_seq
     else:
-        seq_step_ms, spmm_ms = step_ms, spmm_conc_ms
+        seq_step_ms, (spmm_ms, spars_ms) = step_ms, spmm_conc_ms
     total_ms = float(sum(step_ms))
     # max over ranks
     tt = torch.tensor([total_ms], device=device, dtype=torch.float64)
@@ -429,7 +441,10 @@ def bench_sten(args, rank, world, local_rank):
     per_case = []
     for k, c in enumerate(cases):
         t = sum(spmm_ms[k]) / len(spmm_ms[k])
+        ts = sum(spars_ms[k]) / len(spars_ms[k])
         per_case.append({"case": c.label(), "plan": sets[0][k]["plan"].as_dict(), "spmm_us": round(t * 1e3, 2),
+                         "sparsify_us": round(ts * 1e3, 2),
+                         "sparsify_gbs": round(sparsify_bytes(c) / (ts * 1e-3) / 1e9, 1),
                          "spmm_eff_gflops": round(eff_flops(c) / (t * 1e-3) / 1e9, 1),
                          "spmm_nz_tflops": round(nz_flops(c) / (t * 1e-3) / 1e12, 3)})
     out = {
@@ -453,6 +468,14 @@ def bench_sten(args, rank, world, local_rank):
                       "unit": UNIT, "share_of_step": round(spmm_total_ms / sum(seq_step_ms), 4),
                       "single_stream_ms_per_step": round(sum(seq_step_ms) / len(seq_step_ms), 5),
                       "note": "per-launch SpMM times from a second timed pass of the same step on one stream"},
+        "sparsify": {"kernel": "sparsify_grouped_nm_kernel (a1-a3)", "bound": "hbm",
+                     "achieved": round(sum(sparsify_bytes(c) for c in cases) * args.steps
+                                       / (sum(sum(x) for x in spars_ms) * 1e-3) / 1e9, 1),
+                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(sum(sparsify_bytes(c) for c in cases) * args.steps
+                                   / (sum(sum(x) for x in spars_ms) * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+                     "note": "algorithmic bytes M*K*s + M*K'*s + idx per launch over the event-timed launch "
+                             "(single-stream pass; includes the graph node gap)"},
         "per_case": per_case,
         "gpu_launches": launches_per_step * args.steps,
         "loop_ms_device": round(loop_ms, 3),

@@ -9,7 +9,7 @@
 // Mapping: one thread per (group, m-block); consecutive threads take
 // consecutive m-blocks of the same rows, so every warp reads g row segments of
 // 32*m contiguous elements (16-byte vector loads when m*sizeof(T) allows).
-// The first min(8, 32/m) rows of the group stay in registers between the score
+// The first min(4, 32/m) rows of the group stay in registers between the score
 // pass and the compaction pass; later rows are re-read (L1/L2 hits).  HBM roofline:
 // M*K*s (read W) + M*K'*s (values) + (M/g)*(K/m)*n (idx) bytes.
 #pragma once
@@ -17,9 +17,32 @@
 
 namespace sten {
 
+// 256-bit global load (sm_100: LDG.E.ENL2.256): one request per lane for a 32-byte block, so a
+// warp's instruction covers 1 KB contiguous instead of two half-used 512-byte passes.
+STEN_DEVICE_INLINE void ldg256(const void* p, uint32_t (&v)[8]) {
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "l"(p));
+}
+
+// aligned: 0 = element alignment only, 1 = 16-byte, 2 = 32-byte aligned block starts
 template <typename T, int MB>
-STEN_DEVICE_INLINE void load_block(const T* __restrict__ p, T (&row)[MB], bool aligned) {
+STEN_DEVICE_INLINE void load_block(const T* __restrict__ p, T (&row)[MB], int aligned) {
     constexpr int BYTES = MB * int(sizeof(T));
+    if constexpr (BYTES % 32 == 0) {
+        if (aligned == 2) {
+            uint32_t tmp[BYTES / 4];
+#pragma unroll
+            for (int q = 0; q < BYTES / 32; ++q) {
+                uint32_t v[8];
+                ldg256(reinterpret_cast<const unsigned char*>(p) + 32 * q, v);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) tmp[8 * q + e] = v[e];
+            }
+            memcpy(row, tmp, BYTES);
+            return;
+        }
+    }
     if (aligned) {
         if constexpr (BYTES % 16 == 0) {
             uint4 tmp[BYTES / 16];
@@ -73,81 +96,164 @@ STEN_DEVICE_INLINE void store_block(T* __restrict__ p, const T (&row)[MB], bool 
     for (int j = 0; j < MB; ++j) p[j] = row[j];
 }
 
-// rows of a group kept in registers between the two passes (<= 32 elements per thread)
+// rows of a group kept in registers between the two passes (<= 4 rows, <= 32 elements per thread:
+// fewer registers, more resident warps, more loads in flight)
 template <int MB>
-constexpr int sparsify_reg_rows() { return 32 / MB < 1 ? 1 : (32 / MB > 8 ? 8 : 32 / MB); }
+constexpr int sparsify_reg_rows() { return 32 / MB < 1 ? 1 : (32 / MB > 4 ? 4 : 32 / MB); }
 
-template <typename T, int MB>
-__global__ void __launch_bounds__(256)
-sparsify_grouped_nm_kernel(const T* __restrict__ W, int64_t ldw, int64_t G, int64_t KB, int n,
-                           int g, T* __restrict__ values, int64_t Kp, uint8_t* __restrict__ idx,
-                           bool aligned) {
-    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= G * KB) return;
-    const int64_t grp = tid / KB;
-    const int64_t kb = tid - grp * KB;
+template <int BYTES> struct UintOf;
+template <> struct UintOf<1> { using type = uint8_t; };
+template <> struct UintOf<2> { using type = uint16_t; };
+template <> struct UintOf<4> { using type = uint32_t; };
+template <> struct UintOf<8> { using type = uint2; };
+template <> struct UintOf<16> { using type = uint4; };
+
+// Loads of R rows of a group issued back to back (rows >= g are clamped to row 0 and their
+// values ignored), so a thread has R*MB*s bytes in flight instead of one row per DRAM round trip.
+template <typename T, int MB, int R, int ALIGNED>
+STEN_DEVICE_INLINE void load_rows(const T* __restrict__ w0, int64_t ldw, int i0, int g, T (&x)[R][MB]) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int r = i0 + i < g ? i0 + i : 0;
+        load_block<T, MB>(w0 + r * ldw, x[i], ALIGNED);
+    }
+}
+
+// NK = n when n in {1, 2, 4} and the values/idx bases allow NK-element vector stores (the
+// kept entries of a row are selected into registers and written with ONE store per row; the
+// n idx bytes with one store); NK = 0: any n, per-position stores.
+template <typename T, int MB, int NK, int ALIGNED>
+STEN_DEVICE_INLINE void sparsify_body(const T* __restrict__ W, int64_t ldw, int64_t grp, int64_t kb, int64_t KB,
+                                      int n, int g, T* __restrict__ values, int64_t Kp,
+                                      uint8_t* __restrict__ idx) {
     const T* w0 = W + grp * g * ldw + kb * MB;
-    constexpr int kSparsifyRegRows = sparsify_reg_rows<MB>();
+    constexpr int R = sparsify_reg_rows<MB>();
 
     // a1 score: s[j] = fl32(...fl32(|w_0j| + |w_1j|) ... + |w_(g-1)j|), ascending rows, RNE.
     float s[MB];
 #pragma unroll
     for (int j = 0; j < MB; ++j) s[j] = 0.0f;
-    T x[kSparsifyRegRows][MB];
+    T x[R][MB];                                   // rows 0..R-1 stay in registers for a3
+    load_rows<T, MB, R, ALIGNED>(w0, ldw, 0, g, x);
 #pragma unroll
-    for (int i = 0; i < kSparsifyRegRows; ++i) {
+    for (int i = 0; i < R; ++i)
         if (i < g) {
-            load_block<T, MB>(w0 + i * ldw, x[i], aligned);
 #pragma unroll
             for (int j = 0; j < MB; ++j) s[j] = __fadd_rn(s[j], fabsf(to_f32(x[i][j])));
         }
-    }
-    for (int i = kSparsifyRegRows; i < g; ++i) {
-        T row[MB];
-        load_block<T, MB>(w0 + i * ldw, row, aligned);
+    for (int i0 = R; i0 < g; i0 += R) {
+        T y[R][MB];
+        load_rows<T, MB, R, ALIGNED>(w0, ldw, i0, g, y);
 #pragma unroll
-        for (int j = 0; j < MB; ++j) s[j] = __fadd_rn(s[j], fabsf(to_f32(row[j])));
+        for (int i = 0; i < R; ++i)
+            if (i0 + i < g) {
+#pragma unroll
+                for (int j = 0; j < MB; ++j) s[j] = __fadd_rn(s[j], fabsf(to_f32(y[i][j])));
+            }
     }
 
     // a2 select: rank[j] = #{i : s_i > s_j or (s_i == s_j and i < j)}; keep iff rank < n.
+    // The rank rule is the total order (score descending, position ascending), so its n
+    // smallest ranks are found by n passes of an argmax that scans j ascending with a strict
+    // '>' (the first of equal scores wins) over the positions not taken yet: n*MB compares
+    // instead of MB*MB.
     uint32_t keep = 0;
+    const int nsel = NK > 0 ? NK : n;
 #pragma unroll
-    for (int j = 0; j < MB; ++j) {
-        int rank = 0;
+    for (int t = 0; t < (NK > 0 ? NK : MB - 1); ++t) {
+        if (t < nsel) {
+            int bj = -1;
+            float bv = 0.0f;
 #pragma unroll
-        for (int i = 0; i < MB; ++i) rank += (s[i] > s[j]) || (s[i] == s[j] && i < j);
-        keep |= uint32_t(rank < n) << j;
-    }
-
-    // idx: kept positions ascending
-    uint8_t* ip = idx + (grp * KB + kb) * n;
-    {
-        int t = 0;
-#pragma unroll
-        for (int j = 0; j < MB; ++j)
-            if (keep >> j & 1u) ip[t++] = uint8_t(j);
-    }
-
-    // a3 compact: bit copy of the kept entries of every row of the group
-#pragma unroll
-    for (int i = 0; i < kSparsifyRegRows; ++i) {
-        if (i < g) {
-            T* vp = values + (grp * g + i) * Kp + kb * n;
-            int t = 0;
-#pragma unroll
-            for (int j = 0; j < MB; ++j)
-                if (keep >> j & 1u) vp[t++] = x[i][j];
+            for (int j = 0; j < MB; ++j) {
+                const bool better = !(keep >> j & 1u) && (bj < 0 || s[j] > bv);
+                bj = better ? j : bj;
+                bv = better ? s[j] : bv;
+            }
+            keep |= 1u << bj;
         }
     }
-    for (int i = kSparsifyRegRows; i < g; ++i) {
-        T row[MB];
-        load_block<T, MB>(w0 + i * ldw, row, aligned);
-        T* vp = values + (grp * g + i) * Kp + kb * n;
-        int t = 0;
+
+    // kept positions ascending: pos[t] = t-th set bit of keep (exactly n bits are set)
+    constexpr int NP = NK > 0 ? NK : MB - 1;
+    int pos[NP];
+    {
+        uint32_t rem = keep;
 #pragma unroll
-        for (int j = 0; j < MB; ++j)
-            if (keep >> j & 1u) vp[t++] = row[j];
+        for (int t = 0; t < NP; ++t) {
+            pos[t] = __ffs(rem) - 1;
+            rem &= rem - 1u;
+        }
     }
+    // a3 compact: bit copy of the kept entries of row r (select network, then stores)
+    auto select_store = [&](const T (&row)[MB], int64_t r) {
+        T out[NP];
+#pragma unroll
+        for (int t = 0; t < NP; ++t) {
+            T v = row[0];
+#pragma unroll
+            for (int j = 1; j < MB; ++j) v = pos[t] == j ? row[j] : v;
+            out[t] = v;
+        }
+        if constexpr (NK > 0) {
+            using VW = typename UintOf<NK * int(sizeof(T))>::type;
+            VW w;
+            memcpy(&w, out, sizeof(VW));
+            *reinterpret_cast<VW*>(values + r * Kp + kb * NK) = w;
+        } else {
+            T* vp = values + r * Kp + kb * n;
+#pragma unroll
+            for (int t = 0; t < NP; ++t)
+                if (t < n) vp[t] = out[t];
+        }
+    };
+    if constexpr (NK > 0) {
+        using IW = typename UintOf<NK>::type;
+        IW iw;
+        uint8_t ib[NK];
+#pragma unroll
+        for (int t = 0; t < NK; ++t) ib[t] = uint8_t(pos[t]);
+        memcpy(&iw, ib, NK);
+        *reinterpret_cast<IW*>(idx + (grp * KB + kb) * NK) = iw;
+    } else {
+        uint8_t* ip = idx + (grp * KB + kb) * n;
+#pragma unroll
+        for (int t = 0; t < NP; ++t)
+            if (t < n) ip[t] = uint8_t(pos[t]);
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+        if (i < g) select_store(x[i], grp * g + i);
+    for (int i0 = R; i0 < g; i0 += R) {
+        T y[R][MB];
+        load_rows<T, MB, R, ALIGNED>(w0, ldw, i0, g, y);
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+            if (i0 + i < g) select_store(y[i], grp * g + i0 + i);
+    }
+}
+
+template <typename T, int MB, int NK>
+__global__ void __launch_bounds__(256)
+sparsify_grouped_nm_kernel(const T* __restrict__ W, int64_t ldw, int64_t G, int64_t KB, int n,
+                           int g, T* __restrict__ values, int64_t Kp, uint8_t* __restrict__ idx,
+                           int aligned) {
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= G * KB) return;
+    int64_t grp, kb;
+    if (G * KB <= int64_t(0x7fffffff)) {          // 32-bit division (no 64-bit division routine)
+        const uint32_t t32 = uint32_t(tid), kb32 = uint32_t(KB);
+        const uint32_t q = t32 / kb32;
+        grp = q;
+        kb = int64_t(t32 - q * kb32);
+    } else {
+        grp = tid / KB;
+        kb = tid - grp * KB;
+    }
+    // uniform branch: the vector-load body or the scalar one, each with straight-line loads
+    if (aligned == 2) sparsify_body<T, MB, NK, 2>(W, ldw, grp, kb, KB, n, g, values, Kp, idx);
+    else if (aligned == 1) sparsify_body<T, MB, NK, 1>(W, ldw, grp, kb, KB, n, g, values, Kp, idx);
+    else sparsify_body<T, MB, NK, 0>(W, ldw, grp, kb, KB, n, g, values, Kp, idx);
 }
 
 // K2 densify: one thread per (row, m-block); writes the full m-element block

@@ -53,16 +53,33 @@ inline unsigned grid1d(int64_t threads) { return unsigned((threads + 255) / 256)
 // ---------------------------------------------------------------------------------------------
 // K1 / K2 dispatch on (dtype, m)
 // ---------------------------------------------------------------------------------------------
+template <typename T, int MB, int NK>
+void launch_sparsify_nk(const void* W, int64_t ldw, int64_t G, int64_t KB, sten_nmg f, void* values,
+                        int64_t Kp, uint8_t* idx, int aligned, cudaStream_t st) {
+    sparsify_grouped_nm_kernel<T, MB, NK><<<grid1d(G * KB), 256, 0, st>>>(
+        static_cast<const T*>(W), ldw, G, KB, f.n, f.g, static_cast<T*>(values), Kp, idx, aligned);
+}
+
 template <typename T, int MB>
 void launch_sparsify(const void* W, int64_t ldw, int64_t G, int64_t KB, sten_nmg f, void* values,
-                     int64_t Kp, uint8_t* idx, bool aligned, cudaStream_t st) {
-    sparsify_grouped_nm_kernel<T, MB><<<grid1d(G * KB), 256, 0, st>>>(
-        static_cast<const T*>(W), ldw, G, KB, f.n, f.g, static_cast<T*>(values), Kp, idx, aligned);
+                     int64_t Kp, uint8_t* idx, int aligned, cudaStream_t st) {
+    // one vector store per row (n in {1, 2, 4}) when the bases are aligned to the vector width;
+    // every row offset (r Kp + kb n) and idx offset ((G KB + kb) n) is a multiple of n
+    auto ok = [&](int nk) {
+        const uintptr_t va = reinterpret_cast<uintptr_t>(values), ia = reinterpret_cast<uintptr_t>(idx);
+        return f.n == nk && va % (size_t(nk) * sizeof(T)) == 0 && ia % size_t(nk) == 0;
+    };
+    if (ok(1)) launch_sparsify_nk<T, MB, 1>(W, ldw, G, KB, f, values, Kp, idx, aligned, st);
+    else if (ok(2)) launch_sparsify_nk<T, MB, 2>(W, ldw, G, KB, f, values, Kp, idx, aligned, st);
+    else if constexpr (MB > 4) {
+        if (ok(4)) launch_sparsify_nk<T, MB, 4>(W, ldw, G, KB, f, values, Kp, idx, aligned, st);
+        else launch_sparsify_nk<T, MB, 0>(W, ldw, G, KB, f, values, Kp, idx, aligned, st);
+    } else launch_sparsify_nk<T, MB, 0>(W, ldw, G, KB, f, values, Kp, idx, aligned, st);
 }
 
 template <typename T>
 bool dispatch_sparsify(int m, const void* W, int64_t ldw, int64_t G, int64_t KB, sten_nmg f,
-                       void* values, int64_t Kp, uint8_t* idx, bool aligned, cudaStream_t st) {
+                       void* values, int64_t Kp, uint8_t* idx, int aligned, cudaStream_t st) {
     switch (m) {
         case 2: launch_sparsify<T, 2>(W, ldw, G, KB, f, values, Kp, idx, aligned, st); return true;
         case 4: launch_sparsify<T, 4>(W, ldw, G, KB, f, values, Kp, idx, aligned, st); return true;
@@ -404,7 +421,10 @@ sten_status sten_sparsify_grouped_nm(sten_nmg f, sten_dtype dt, const void* W, i
     if (M * K > 0 && (!W || !values || !idx)) return STEN_ERR_INVALID_ARG;
     const int64_t G = M / f.g, KB = K / f.m, Kp = KB * f.n;
     if (G == 0 || KB == 0) return STEN_OK;
-    const bool aligned = aligned16(W) && (ldw * int64_t(dt_size(dt))) % 16 == 0;
+    // 2: 32-byte aligned block starts (256-bit loads when m*s is a multiple of 32), 1: 16-byte
+    const int64_t ldw_bytes = ldw * int64_t(dt_size(dt));
+    const uintptr_t wa = reinterpret_cast<uintptr_t>(W);
+    const int aligned = (wa % 32 == 0 && ldw_bytes % 32 == 0) ? 2 : (wa % 16 == 0 && ldw_bytes % 16 == 0) ? 1 : 0;
     cudaStream_t st = as_stream(stream);
     bool ok = dt == STEN_F32 ? dispatch_sparsify<float>(f.m, W, ldw, G, KB, f, values, Kp, idx, aligned, st)
                              : dispatch_sparsify<bf16_t>(f.m, W, ldw, G, KB, f, values, Kp, idx, aligned, st);

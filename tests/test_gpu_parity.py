@@ -85,6 +85,30 @@ def test_sparsify_unaligned_ld_and_integer_ties():
     assert np.array_equal(host(i), oracle.brute_select(W, n, m, g))
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n,m", [(1, 8), (2, 8), (4, 8), (2, 4), (1, 16), (3, 6)])
+@pytest.mark.parametrize("ld_multiple", [1, 4, 8, 16])
+@pytest.mark.parametrize("out_offset", [0, 1])
+def test_sparsify_load_and_store_paths(dtype, n, m, ld_multiple, out_offset):
+    """Every load width (scalar / 16-byte / 256-bit, chosen by the W base and ldw) and both
+    store forms (one vector store per row when values/idx bases allow n-element vectors, else
+    per-position stores: out_offset = 1 misaligns both outputs) give the oracle's bytes."""
+    g, M, K = 4, 24, 41 * m
+    W = synthetic.weights(M, K, seed=7 * n + m + ld_multiple, dtype=dtype)
+    Wt = dev(W, dtype, ld_multiple=ld_multiple)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    kept = K // m * n
+    vbuf = torch.empty(M * kept + 1, dtype=tdt, device="cuda")
+    ibuf = torch.empty((M // g) * (K // m) * n + 1, dtype=torch.uint8, device="cuda")
+    v = vbuf[out_offset:out_offset + M * kept].view(M, kept)
+    i = ibuf[out_offset:out_offset + (M // g) * (K // m) * n].view(M // g, K // m, n)
+    sten.sparsify_grouped_nm(Wt, n, m, g, values=v, idx=i)
+    torch.cuda.synchronize()
+    v_ref, i_ref = oracle.sparsify(W, n, m, g)
+    assert np.array_equal(host(i), i_ref)
+    assert np.array_equal(host(v).view(np.uint8), v_ref.view(np.uint8))
+
+
 def test_sparsify_large_group_and_fp32_near_ties():
     n, m, g = 1, 2, 3
     e = np.float32(2.0 ** -24)
