@@ -124,8 +124,11 @@ spmm_mma_kernel(const SpmmArgs a) {
     const int warp = tid >> 5, lane = tid & 31;
     const int64_t n0 = int64_t(blockIdx.x) * BN;
     const int64_t m0 = int64_t(blockIdx.y) * BM;
-    const int64_t kb_begin = int64_t(blockIdx.z) * a.kb_per_split;
-    const int64_t kb_end = min64(a.KB, kb_begin + a.kb_per_split);
+    // split-K part z = blockIdx.z owns slabs [z T / S, (z+1) T / S) of the T slabs (balanced: the
+    // parts differ by at most one slab, so no CTA of the cluster idles at the reduction barrier)
+    const int64_t tot_slabs = (a.KB + kbs - 1) / kbs;
+    const int64_t kb_begin = (tot_slabs * int64_t(blockIdx.z) / a.split) * kbs;
+    const int64_t kb_end = min64(a.KB, (tot_slabs * int64_t(blockIdx.z + 1) / a.split) * kbs);
     const int nslabs = kb_end > kb_begin ? int((kb_end - kb_begin + kbs - 1) / kbs) : 0;
 
     auto sB = [&](int buf) { return smem + L.stages + size_t(buf) * L.stage; };
@@ -349,9 +352,8 @@ inline cudaError_t launch_mma_cfg(SpmmArgs a, int split, cudaStream_t st) {
     using Cfg = MmaCfg<RB, MR, SUB, WARPS>;
     a.kbs = mma_slab_blocks<RB, MR, SUB, WARPS>(a.n, a.m);
     const int64_t slabs = (a.KB + a.kbs - 1) / a.kbs;
-    const int64_t per = (slabs + split - 1) / split;
-    a.kb_per_split = per * a.kbs;
-    a.split = int((a.KB + a.kb_per_split - 1) / a.kb_per_split);
+    a.split = int(slabs < split ? slabs : split);                 // balanced whole-slab parts
+    a.kb_per_split = ((slabs + a.split - 1) / a.split) * a.kbs;  // largest part (informational)
     const size_t smem = mma_smem<RB, MR, SUB, WARPS>(a.kbs, a.n, a.m);
     if (smem > 232448) return cudaErrorInvalidValue;
     auto kern = spmm_mma_kernel<TC, RB, MR, SUB, WARPS>;

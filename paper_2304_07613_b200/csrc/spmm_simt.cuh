@@ -275,8 +275,8 @@ STEN_DEVICE_INLINE void cluster_reduce_store(unsigned char* tile_smem, const Spm
 // A consumer waits on the full barrier, turns its sub-blocks' idx bytes into shared
 // addresses of staged B rows (warp-private), runs the LDS/FFMA2 loop and arrives on
 // the empty barrier.  No CTA-wide barrier per slab.
-template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1)
+template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
 spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmV) {
     using Cfg = SimtCfg<TAB, RG, TN, SUB, WARPS>;
     constexpr int EV = Cfg::kEV;
@@ -301,8 +301,11 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
     const int warp = tid >> 5, lane = tid & 31;
     const int64_t n0 = int64_t(blockIdx.x) * BN;
     const int64_t m0 = int64_t(blockIdx.y) * BM;
-    const int64_t kb_begin = int64_t(blockIdx.z) * a.kb_per_split;
-    const int64_t kb_end = min64(a.KB, kb_begin + a.kb_per_split);
+    // split-K part z = blockIdx.z owns slabs [z T / S, (z+1) T / S) of the T slabs (balanced: the
+    // parts differ by at most one slab, so no CTA of the cluster idles at the reduction barrier)
+    const int64_t tot_slabs = (a.KB + kbs - 1) / kbs;
+    const int64_t kb_begin = (tot_slabs * int64_t(blockIdx.z) / a.split) * kbs;
+    const int64_t kb_end = min64(a.KB, (tot_slabs * int64_t(blockIdx.z + 1) / a.split) * kbs);
     const int nslabs = kb_end > kb_begin ? int((kb_end - kb_begin + kbs - 1) / kbs) : 0;
 
     auto sB = [&](int buf) { return smem + L.stages + size_t(buf) * L.stage; };

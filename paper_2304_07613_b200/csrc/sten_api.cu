@@ -132,9 +132,12 @@ int simt_rows_per_warp(int g) {
 // and two narrow tiles for small grids (more CTAs per output without split-K), fp32 only:
 //   4: 8 warps,  TN = 4, BM = 112, BN = 128 (64 accumulators)    -- 2 CTAs / SM
 //   5: 8 warps,  TN = 4, BM = 56,  BN = 128 (32 accumulators)    -- 2 CTAs / SM
-struct SimtTile { int warps, tn, bm; };
-constexpr SimtTile kSimtTiles[6] = {{0, 0, 0}, {8, 8, 56}, {16, 8, 120}, {16, 4, 240}, {8, 4, 112}, {8, 4, 56}};
-constexpr int kSimtNumTiles = 5;
+//   6: 8 warps,  TN = 4, BM = 56,  BN = 128 (32 accumulators)    -- 3 CTAs / SM (21 consumer warps)
+//   7: 12 warps, TN = 4, BM = 88,  BN = 128 (32 accumulators)    -- 2 CTAs / SM (22 consumer warps)
+struct SimtTile { int warps, tn, bm, per_sm; };
+constexpr SimtTile kSimtTiles[8] = {{0, 0, 0, 0},   {8, 8, 56, 2}, {16, 8, 120, 1}, {16, 4, 240, 1},
+                                    {8, 4, 112, 2}, {8, 4, 56, 2}, {8, 4, 56, 3},   {12, 4, 88, 2}};
+constexpr int kSimtNumTiles = 7;
 constexpr int kMaxSplit = 8;              // portable thread-block cluster size
 
 inline bool simt_tile_ok(int tile, sten_dtype ab) {
@@ -145,7 +148,8 @@ inline bool simt_tile_ok(int tile, sten_dtype ab) {
 // Shared-memory budget per CTA: tiles 1, 4, 5 run two CTAs per SM, tiles 2/3 one.
 constexpr size_t kSmemPerSM = 233472;                                    // 228 KB
 inline size_t simt_smem_budget(int tile) {
-    return (tile == 1 || tile >= 4) ? kSmemPerSM / 2 - 1024 : 232448;
+    const int per_sm = kSimtTiles[tile].per_sm;
+    return per_sm == 1 ? 232448 : kSmemPerSM / per_sm - 1024;
 }
 
 // m-blocks per K-slab for the SIMT kernel: the largest multiple of 4/gcd(n,4) whose
@@ -167,7 +171,7 @@ int simt_slab_blocks(sten_nmg f, sten_dtype ab, int tile) {
     return best;
 }
 
-template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS>
+template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS, int MINB = (WARPS == 8 ? 2 : 1)>
 sten_status launch_simt_cfg(SpmmArgs a, cudaStream_t st) {
     using Cfg = SimtCfg<TAB, RG, TN, SUB, WARPS>;
     const SimtSmem<TAB, RG, TN, SUB, WARPS> L(a.kbs, a.n, a.m);
@@ -185,7 +189,7 @@ sten_status launch_simt_cfg(SpmmArgs a, cudaStream_t st) {
     a.v_tma = KU * s == 16 && (size_t(a.Kp) * s) % 16 == 0 && aligned16(a.values) &&
               make_tmap_3d(&tmV, a.values, tdt, uint64_t(KU), uint64_t(a.M), uint64_t(a.Kp / KU),
                            uint64_t(a.Kp) * s, uint64_t(KU) * s, uint32_t(KU), Cfg::kBM, uint32_t(L.ksp / KU));
-    auto kern = spmm_simt_kernel<TAB, TC, RG, TN, SUB, WARPS>;
+    auto kern = spmm_simt_kernel<TAB, TC, RG, TN, SUB, WARPS, MINB>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total)) != cudaSuccess)
         return STEN_ERR_CUDA;
     cudaLaunchConfig_t cfg = {};
@@ -219,6 +223,12 @@ sten_status launch_simt_rg(const SpmmArgs& a, int tile, cudaStream_t st) {
             else return STEN_ERR_UNSUPPORTED;
         case 5:
             if constexpr (sizeof(TAB) == 4) return launch_simt_cfg<TAB, TC, RG, 4, SUB8, 8>(a, st);
+            else return STEN_ERR_UNSUPPORTED;
+        case 6:
+            if constexpr (sizeof(TAB) == 4) return launch_simt_cfg<TAB, TC, RG, 4, SUB8, 8, 3>(a, st);
+            else return STEN_ERR_UNSUPPORTED;
+        case 7:
+            if constexpr (sizeof(TAB) == 4) return launch_simt_cfg<TAB, TC, RG, 4, SUB8, 12, 2>(a, st);
             else return STEN_ERR_UNSUPPORTED;
     }
     return STEN_ERR_UNSUPPORTED;
@@ -380,11 +390,10 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
         a.v_async = (a.Kp % 4 == 0) && ((reinterpret_cast<uintptr_t>(values) & (4 * sab - 1)) == 0);
         a.idx_bytes = (M / f.g) * a.KB * f.n;
         a.kbs = simt_slab_blocks(f, ab_dt, plan.tile);
-        // split-K parts are whole slabs; S = ceil(KB / per-part)
+        // split-K parts are balanced runs of whole slabs (sizes differ by at most one slab)
         const int64_t slabs = (a.KB + a.kbs - 1) / a.kbs;
-        const int64_t per = (slabs + plan.split_k - 1) / plan.split_k;
-        a.kb_per_split = per * a.kbs;
-        a.split = int((a.KB + a.kb_per_split - 1) / a.kb_per_split);
+        a.split = int(slabs < plan.split_k ? slabs : plan.split_k);
+        a.kb_per_split = ((slabs + a.split - 1) / a.split) * a.kbs;   // largest part (informational)
         if (ab_dt == STEN_F32) s = c_dt == STEN_F32 ? launch_simt<float, float>(a, plan.tile, st)
                                                     : launch_simt<float, bf16_t>(a, plan.tile, st);
         else s = c_dt == STEN_F32 ? launch_simt<bf16_t, float>(a, plan.tile, st)

@@ -136,7 +136,7 @@ def test_p0_worked_example_on_gpu(golden_dir):
 # ----------------------------------------------------------------------------------------
 # SpMM parity on every algorithm / tile / split
 # ----------------------------------------------------------------------------------------
-SIMT_TILES = [1, 2, 3, 4, 5]
+SIMT_TILES = [1, 2, 3, 4, 5, 6, 7]
 
 
 def _spmm_case(M, K, N, n, m, g, dtype, plan=None, out_dtype=None, seed=0):
