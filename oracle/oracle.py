@@ -50,6 +50,11 @@ def _load():
         lib.oracle_dense_matmul.argtypes = [ctypes.c_int, _ptr, _i64, _i64, _i64, _ptr, _i64, _i64,
                                             _ptr, ctypes.c_int]
         lib.oracle_energy.argtypes = [ctypes.c_int, _ptr, _ptr, _i64, _i64, _i64]
+        lib.oracle_nmg_patterns.argtypes = [ctypes.c_int, ctypes.c_int, _ptr]
+        lib.oracle_nmg_sparsify.argtypes = [ctypes.c_int] * 4 + [_ptr, _i64, _i64, _i64, _ptr, _ptr]
+        lib.oracle_nmg_densify.argtypes = [ctypes.c_int] * 4 + [_ptr, _ptr, _i64, _i64, _ptr, _i64]
+        lib.oracle_nmg_spmm.argtypes = [ctypes.c_int] * 4 + [_ptr, _ptr, _i64, _i64, _ptr, _i64, _i64,
+                                                             _ptr, _ptr, ctypes.c_int]
         lib.oracle_energy.restype = ctypes.c_double
         for f in (lib.oracle_sparsify, lib.oracle_densify, lib.oracle_spmm, lib.oracle_dense_matmul):
             f.restype = ctypes.c_int
@@ -172,3 +177,90 @@ def brute_select(W_int: np.ndarray, n: int, m: int, g: int) -> np.ndarray:
                     best, best_sum = subset, tot
             out[grp, kb] = best
     return out
+
+
+# ---------------------------------------------------------------------------------------------
+# Chunked n:m:g -- the paper's own format (R17-R21)
+# ---------------------------------------------------------------------------------------------
+def nmg_patterns(n: int, m: int) -> np.ndarray:
+    """The C(m,n) patterns in the fixed (revolving-door) order: [C][n] ascending positions."""
+    C = comb(m, n)
+    pos = np.zeros((C, n), dtype=np.int32)
+    _check(_load().oracle_nmg_patterns(n, m, _p(pos)), "nmg_patterns")
+    return pos
+
+
+def comb(m: int, n: int) -> int:
+    import math
+    return math.comb(m, n)
+
+
+def nmg_chunk(n: int, m: int, g: int) -> int:
+    """L = C(m,n) * g columns per chunk."""
+    return comb(m, n) * g
+
+
+def nmg_sparsify(W: np.ndarray, n: int, m: int, g: int):
+    """Greedy conversion to chunked n:m:g: (values [M/m][K/L][L][n], idx [M/m][K/L][L] uint16)."""
+    W = np.ascontiguousarray(W)
+    M, K = W.shape
+    L = nmg_chunk(n, m, g)
+    if M % m or K % L:
+        raise ValueError("shape (%d, %d) not divisible by m=%d / L=%d" % (M, K, m, L))
+    values = np.zeros((M // m, K // L, L, n), dtype=W.dtype)
+    idx = np.zeros((M // m, K // L, L), dtype=np.uint16)
+    _check(_load().oracle_nmg_sparsify(n, m, g, _dtype_code(W), _p(W), M, K, K, _p(values), _p(idx)),
+           "nmg_sparsify")
+    return values, idx
+
+
+def nmg_densify(values: np.ndarray, idx: np.ndarray, n: int, m: int, g: int, K: int) -> np.ndarray:
+    values = np.ascontiguousarray(values)
+    idx = np.ascontiguousarray(idx, dtype=np.uint16)
+    M = values.shape[0] * m
+    out = np.empty((M, K), dtype=values.dtype)
+    _check(_load().oracle_nmg_densify(n, m, g, _dtype_code(values), _p(values), _p(idx), M, K, _p(out), K),
+           "nmg_densify")
+    return out
+
+
+def nmg_spmm(values: np.ndarray, idx: np.ndarray, B: np.ndarray, n: int, m: int, g: int, nthreads: int = 1):
+    """fp64 C = mask(W) @ B for chunked n:m:g, and Bound = |mask(W)| @ |B|."""
+    values = np.ascontiguousarray(values)
+    idx = np.ascontiguousarray(idx, dtype=np.uint16)
+    B = np.ascontiguousarray(B)
+    if B.dtype != values.dtype:
+        raise TypeError("values and B must share a dtype")
+    M = values.shape[0] * m
+    K, N = B.shape
+    C = np.zeros((M, N), dtype=np.float64)
+    Bd = np.zeros_like(C)
+    _check(_load().oracle_nmg_spmm(n, m, g, _dtype_code(values), _p(values), _p(idx), M, K, _p(B), N, N,
+                                   _p(C), _p(Bd), nthreads), "nmg_spmm")
+    return C, Bd
+
+
+def nmg_brute_best_energy(W_int: np.ndarray, n: int, m: int, g: int) -> float:
+    """Exhaustive optimum of the L1 objective over every valid chunked
+    n:m:g mask of a tiny integer W (one row block, one chunk): every assignment of the L
+    columns to patterns with each pattern used exactly g times.  Returns the kept L1 mass."""
+    W = np.abs(np.asarray(W_int, dtype=np.float64))
+    M, K = W.shape
+    L = nmg_chunk(n, m, g)
+    assert M == m and K == L
+    pats = list(itertools.combinations(range(m), n))
+    best = -1.0
+
+    def rec(b, cnt, tot):
+        nonlocal best
+        if b == L:
+            best = max(best, tot)
+            return
+        for p, P in enumerate(pats):
+            if cnt[p] < g:
+                cnt[p] += 1
+                rec(b + 1, cnt, tot + sum(W[i, b] for i in P))
+                cnt[p] -= 1
+
+    rec(0, [0] * len(pats), 0.0)
+    return best

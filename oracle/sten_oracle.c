@@ -224,3 +224,209 @@ int oracle_max_threads(void)
     return 1;
 #endif
 }
+
+/* ==========================================================================
+ * Chunked n:m:g -- the paper's own format (DESIGN.md
+ * readings R17-R21).  Test infrastructure, like everything in this file.
+ *
+ *   "each nonzero pattern is repeated g times, forming a group ... we combine
+ *    groups into chunks with all C(m,n) combinations of nonzeros in fixed
+ *    order ... we permit reordering the blocks of m elements within each
+ *    chunk, and so store an index encoding the original location of each
+ *    block"
+ *   "The permutation order in chunks is selected so the nonzero pattern
+ *    between adjacent groups differs in only one location"
+ *   CPU conversion: "compute the total magnitude of the preserved elements for
+ *    each column of a chunk with all permutations of nonzero patterns ...
+ *    C(m,n)^2 g such columnwise magnitudes.  This list is then sorted and
+ *    processed from highest to lowest.  We use a specific nonzero pattern for a
+ *    column ... only if this column was not yet selected and the group
+ *    corresponding to the pattern is not yet full."
+ *   densify: "a single iteration over the values, reordering their location
+ *    according to the stored index"
+ *
+ * Readings (paper silent): R17 a block ("column" of a chunk) is m consecutive
+ * rows of W at one input column k -- the m-blocks run along the output rows M
+ * and the chunks along K, L = C(m,n) g consecutive columns per chunk; R18 the
+ * fixed pattern order is the revolving-door order R(m,n) = R(m-1,n) followed by
+ * reverse(R(m-1,n-1)) each with m-1 added (adjacent patterns differ in one
+ * element in, one out); R19 magnitude of (column b, pattern p) = fp32 sum of
+ * |w| over p's positions ascending; ties in the sorted list by column
+ * ascending, then pattern id ascending; R20 within a group (pattern) the g
+ * columns are stored in ascending original column order; R21 idx is uint16.
+ *
+ * Layouts:  W [M][ldw]; values [M/m][K/L][L][n]; idx [M/m][K/L][L] (uint16,
+ * original column offset in the chunk); slot s of a chunk has pattern s / g.
+ * ========================================================================== */
+
+static int nmg_binom(int m, int n)
+{
+    if (n < 0 || n > m) return 0;
+    long r = 1;
+    for (int i = 1; i <= n; ++i) r = r * (m - n + i) / i;
+    return (int)r;
+}
+
+/* Revolving-door list R(m, n) of n-subsets of {0..m-1}, written as bitmasks
+ * into out[0 .. C(m,n)-1]; returns the count.  Recursive definition (R18). */
+static int nmg_revolving_door(int m, int n, uint32_t* out)
+{
+    if (n == 0) { out[0] = 0u; return 1; }
+    if (n == m) { out[0] = (m >= 32) ? 0xffffffffu : ((1u << m) - 1u); return 1; }
+    int a = nmg_revolving_door(m - 1, n, out);
+    uint32_t* tmp = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)nmg_binom(m - 1, n - 1));
+    int b = nmg_revolving_door(m - 1, n - 1, tmp);
+    for (int i = 0; i < b; ++i) out[a + i] = tmp[b - 1 - i] | (1u << (m - 1));
+    free(tmp);
+    return a + b;
+}
+
+/* Patterns as ascending position lists: pos[p*n + t]. */
+int oracle_nmg_patterns(int n, int m, int32_t* pos)
+{
+    if (n < 1 || n >= m || m > 16) return 1;
+    int C = nmg_binom(m, n);
+    uint32_t* mask = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)C);
+    nmg_revolving_door(m, n, mask);
+    for (int p = 0; p < C; ++p) {
+        int t = 0;
+        for (int j = 0; j < m; ++j)
+            if (mask[p] >> j & 1u) pos[p * n + t++] = j;
+    }
+    free(mask);
+    return 0;
+}
+
+static int nmg_check(int n, int m, int g, int dtype, int64_t M, int64_t K)
+{
+    if (n < 1 || n >= m || m > 16 || g < 1 || (dtype != 0 && dtype != 1) || M < 0 || K < 0) return 1;
+    int64_t L = (int64_t)nmg_binom(m, n) * g;
+    if (L > 65535) return 1;
+    if (M % m != 0 || K % L != 0) return 2;
+    return 0;
+}
+
+/* Greedy conversion of one chunk, sorted list processed in
+ * order (magnitude desc, column asc, pattern asc). */
+int oracle_nmg_sparsify(int n, int m, int g, int dtype,
+                        const void* W, int64_t M, int64_t K, int64_t ldw,
+                        void* values, uint16_t* idx)
+{
+    int rc = nmg_check(n, m, g, dtype, M, K);
+    if (rc) return rc;
+    if (ldw < K) return 2;
+    const int C = nmg_binom(m, n);
+    const int64_t L = (int64_t)C * g, NC = K / L, RB = M / m;
+    int32_t* pos = (int32_t*)malloc(sizeof(int32_t) * (size_t)C * n);
+    oracle_nmg_patterns(n, m, pos);
+    const int64_t NI = L * C;
+    float* mag = (float*)malloc(sizeof(float) * (size_t)NI);
+    int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)NI);
+    int* pat_of = (int*)malloc(sizeof(int) * (size_t)L);
+    int* cnt = (int*)malloc(sizeof(int) * (size_t)C);
+    for (int64_t rb = 0; rb < RB; ++rb)
+        for (int64_t c = 0; c < NC; ++c) {
+            /* item i = b*C + p: magnitude of column b under pattern p */
+            for (int64_t b = 0; b < L; ++b)
+                for (int p = 0; p < C; ++p) {
+                    float s = 0.0f;
+                    for (int t = 0; t < n; ++t)
+                        s = s + fabsf(widen(dtype, W, (rb * m + pos[p * n + t]) * ldw + c * L + b));
+                    mag[b * C + p] = s;
+                }
+            /* sort: insertion sort by (mag desc, b asc, p asc) -- plain and obviously correct */
+            for (int64_t i = 0; i < NI; ++i) order[i] = i;
+            for (int64_t i = 1; i < NI; ++i) {
+                int64_t x = order[i], j = i - 1;
+                while (j >= 0 && (mag[order[j]] < mag[x] ||
+                                  (mag[order[j]] == mag[x] && order[j] > x))) {
+                    order[j + 1] = order[j];
+                    --j;
+                }
+                order[j + 1] = x;
+            }
+            /* process from highest to lowest */
+            for (int64_t b = 0; b < L; ++b) pat_of[b] = -1;
+            for (int p = 0; p < C; ++p) cnt[p] = 0;
+            for (int64_t i = 0; i < NI; ++i) {
+                int64_t b = order[i] / C;
+                int p = (int)(order[i] % C);
+                if (pat_of[b] < 0 && cnt[p] < g) { pat_of[b] = p; cnt[p]++; }
+            }
+            /* store: slot s = p*g + (rank of b among the columns of pattern p, ascending b) */
+            for (int p = 0; p < C; ++p) {
+                int64_t s = (int64_t)p * g;
+                for (int64_t b = 0; b < L; ++b)
+                    if (pat_of[b] == p) {
+                        int64_t slot = (rb * NC + c) * L + s;
+                        idx[slot] = (uint16_t)b;
+                        for (int t = 0; t < n; ++t)
+                            copy_elem(dtype, values, slot * n + t, W, (rb * m + pos[p * n + t]) * ldw + c * L + b);
+                        ++s;
+                    }
+            }
+        }
+    free(pos); free(mag); free(order); free(pat_of); free(cnt);
+    return 0;
+}
+
+int oracle_nmg_densify(int n, int m, int g, int dtype, const void* values, const uint16_t* idx,
+                       int64_t M, int64_t K, void* W_out, int64_t ldw)
+{
+    int rc = nmg_check(n, m, g, dtype, M, K);
+    if (rc) return rc;
+    if (ldw < K) return 2;
+    const int C = nmg_binom(m, n);
+    const int64_t L = (int64_t)C * g, NC = K / L, RB = M / m;
+    int32_t* pos = (int32_t*)malloc(sizeof(int32_t) * (size_t)C * n);
+    oracle_nmg_patterns(n, m, pos);
+    for (int64_t r = 0; r < M; ++r)
+        for (int64_t k = 0; k < K; ++k) zero_elem(dtype, W_out, r * ldw + k);
+    for (int64_t rb = 0; rb < RB; ++rb)
+        for (int64_t c = 0; c < NC; ++c)
+            for (int64_t s = 0; s < L; ++s) {
+                int64_t slot = (rb * NC + c) * L + s;
+                int p = (int)(s / g);
+                for (int t = 0; t < n; ++t)
+                    copy_elem(dtype, W_out, (rb * m + pos[p * n + t]) * ldw + c * L + idx[slot], values, slot * n + t);
+            }
+    free(pos);
+    return 0;
+}
+
+/* C[r][c] = sum over chunks, slots, kept t (fp64, storage order); Bound = sum |v||b|. */
+int oracle_nmg_spmm(int n, int m, int g, int dtype, const void* values, const uint16_t* idx,
+                    int64_t M, int64_t K, const void* B, int64_t ldb, int64_t N,
+                    double* Cout, double* Bound, int nthreads)
+{
+    int rc = nmg_check(n, m, g, dtype, M, K);
+    if (rc) return rc;
+    if (ldb < N) return 2;
+    const int C = nmg_binom(m, n);
+    const int64_t L = (int64_t)C * g, NC = K / L, RB = M / m;
+    int32_t* pos = (int32_t*)malloc(sizeof(int32_t) * (size_t)C * n);
+    oracle_nmg_patterns(n, m, pos);
+    for (int64_t i = 0; i < M * N; ++i) { Cout[i] = 0.0; if (Bound) Bound[i] = 0.0; }
+#ifdef _OPENMP
+    if (nthreads < 1) nthreads = 1;
+#pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1)
+#endif
+    for (int64_t rb = 0; rb < RB; ++rb)
+        for (int64_t c = 0; c < NC; ++c)
+            for (int64_t s = 0; s < L; ++s) {
+                int64_t slot = (rb * NC + c) * L + s;
+                int64_t k = c * L + idx[slot];
+                int p = (int)(s / g);
+                for (int t = 0; t < n; ++t) {
+                    int64_t r = rb * m + pos[p * n + t];
+                    double v = (double)widen(dtype, values, slot * n + t);
+                    for (int64_t col = 0; col < N; ++col) {
+                        double b = (double)widen(dtype, B, k * ldb + col);
+                        Cout[r * N + col] += v * b;
+                        if (Bound) Bound[r * N + col] += fabs(v) * fabs(b);
+                    }
+                }
+            }
+    free(pos);
+    return 0;
+}
