@@ -158,6 +158,53 @@ sten_status sten_sparse_linear_host(sten_nmg f, sten_dtype ab_dt,
                                     void* C_host, int64_t ldc, sten_dtype c_dt,
                                     void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Chunked n:m:g -- the paper's own format (
+ * DESIGN.md readings R17-R21).
+ *
+ *   A "column" is one block of m consecutive ROWS of W at one input column k
+ *   (the m-blocks run along the output rows M); a chunk is L = C(m,n) g
+ *   consecutive columns k of one row block.  Every one of the C(m,n) nonzero
+ *   patterns is used by exactly g columns of a chunk ("each nonzero pattern is
+ *   repeated g times, forming a group ... chunks with all C(m,n) combinations
+ *   of nonzeros in fixed order").  The fixed order is the
+ *   revolving-door order (adjacent patterns differ in one position).
+ *   Columns are reordered inside the chunk: slot s holds a column of pattern
+ *   s / g, the g columns of a pattern in ascending original position, and idx
+ *   stores each slot's original column offset in the chunk.
+ *
+ *   values [M/m][K/L][L][n]  dtype dt; values[rb][c][s][t] = W[rb m + pos_t(s/g)][c L + idx[rb][c][s]]
+ *   idx    [M/m][K/L][L]     uint16
+ *
+ *   Conversion = the paper's CPU greedy, computed exactly on
+ *   the GPU: the C(m,n)^2 g (column, pattern) magnitudes of a chunk (fp32 sums of
+ *   |w| over the pattern's positions, ascending) processed from highest to lowest
+ *   (ties: lower column, then lower pattern id), a column taking a pattern if
+ *   it is unassigned and the pattern has < g columns.
+ *
+ *   Shapes: M % m == 0 and K % L == 0 (else STEN_ERR_SHAPE; the caller pads);
+ *   1 <= n < m <= 16, C(m,n) <= 64 and L * C(m,n) <= 2048 (else
+ *   STEN_ERR_UNSUPPORTED).  The SpMM is compiled for (n, m) in {1:2, 1:4, 2:4,
+ *   1:8} and fp32 / bf16 inputs (fp32 accumulate); other formats convert and
+ *   densify but their product returns STEN_ERR_UNSUPPORTED.  Pointers, streams,
+ *   ownership and error behaviour as for the grouped n:m calls above.
+ * --------------------------------------------------------------------------- */
+sten_status sten_nmg_sparsify(sten_nmg f, sten_dtype dt,
+                              const void* W, int64_t M, int64_t K, int64_t ldw,
+                              void* values, uint16_t* idx, void* stream);
+
+/* to dense: W_out [M][ldw], zeros at pruned positions. */
+sten_status sten_nmg_densify(sten_nmg f, sten_dtype dt,
+                             const void* values, const uint16_t* idx, int64_t M, int64_t K,
+                             void* W_out, int64_t ldw, void* stream);
+
+/* C = densify(values, idx) x B (Fig. 5): B [K][ldb] ab_dt,
+ * C [M][ldc] c_dt, overwritten.  B base and ldb 16-byte aligned. */
+sten_status sten_nmg_spmm(sten_nmg f, sten_dtype ab_dt,
+                          const void* values, const uint16_t* idx, int64_t M, int64_t K,
+                          const void* B, int64_t ldb, int64_t N,
+                          void* C, int64_t ldc, sten_dtype c_dt, void* stream);
+
 const char* sten_status_string(sten_status s);
 const char* sten_algo_name(int32_t algo);
 /* Number of kernel launches the last call of each entry point enqueues is

@@ -1,0 +1,146 @@
+// nmg_api.cu -- C ABI of the chunked n:m:g format (include/sten.h, "Chunked n:m:g"):
+// argument validation, pattern table, kernel instantiation and launch.
+#include "sten.h"
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "nmg.cuh"
+
+using namespace sten;
+
+namespace {
+
+inline cudaStream_t nmg_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline bool nmg_dtype_ok(int d) { return d == STEN_F32 || d == STEN_BF16; }
+inline size_t nmg_dt_size(sten_dtype d) { return d == STEN_F32 ? 4 : 2; }
+inline sten_status nmg_last_cuda() { return cudaGetLastError() == cudaSuccess ? STEN_OK : STEN_ERR_CUDA; }
+
+// format + shape checks shared by the three calls; fills the kernel arguments
+sten_status nmg_setup(sten_nmg f, int dt, int64_t M, int64_t K, NmgArgs* a) {
+    if (f.n < 1 || f.n >= f.m || f.m > 16 || f.g < 1 || !nmg_dtype_ok(dt)) return STEN_ERR_INVALID_ARG;
+    const int C = nmg_binom(f.m, f.n);
+    if (C > kNmgMaxPatterns) return STEN_ERR_UNSUPPORTED;
+    const int64_t L = int64_t(C) * f.g;
+    if (L > 65535 || L * C > 2048) return STEN_ERR_UNSUPPORTED;
+    if (M < 0 || K < 0 || M % f.m != 0 || K % L != 0) return STEN_ERR_SHAPE;
+    a->n = f.n; a->m = f.m; a->g = f.g; a->C = C; a->L = int(L);
+    a->M = M; a->K = K; a->NC = K / L; a->RB = M / f.m;
+    a->pat = nmg_revolving_door(f.m, f.n);
+    return STEN_OK;
+}
+
+template <typename TAB, typename TC, int NN, int MM>
+sten_status launch_nmg_spmm(const NmgSpmmArgs& a0, cudaStream_t st) {
+    constexpr int RBW = MM <= 4 ? 2 : 1;
+    NmgSpmmArgs a = a0;
+    a.cps = a.L >= 64 ? 1 : (64 + a.L - 1) / a.L;                   // >= 64 B rows per K-stage
+    if (a.cps > a.NC) a.cps = int(a.NC > 0 ? a.NC : 1);
+    const size_t smem = 2 * nmg_spmm_stage_bytes<TAB>(a.cps * a.L);
+    if (smem > 227 * 1024) return STEN_ERR_UNSUPPORTED;
+    auto kern = nmg_spmm_kernel<TAB, TC, NN, MM, RBW>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+        return STEN_ERR_CUDA;
+    const int64_t rb_per_cta = int64_t(kNmgSpmmWarps) * RBW;
+    dim3 grid(unsigned((a.N + kNmgBN - 1) / kNmgBN), unsigned((a.RB + rb_per_cta - 1) / rb_per_cta));
+    kern<<<grid, kNmgSpmmWarps * 32, smem, st>>>(a);
+    return nmg_last_cuda();
+}
+
+template <typename TAB, typename TC>
+sten_status dispatch_nmg_spmm(int n, int m, const NmgSpmmArgs& a, cudaStream_t st) {
+    if (n == 1 && m == 2) return launch_nmg_spmm<TAB, TC, 1, 2>(a, st);
+    if (n == 1 && m == 4) return launch_nmg_spmm<TAB, TC, 1, 4>(a, st);
+    if (n == 2 && m == 4) return launch_nmg_spmm<TAB, TC, 2, 4>(a, st);
+    if (n == 1 && m == 8) return launch_nmg_spmm<TAB, TC, 1, 8>(a, st);
+    return STEN_ERR_UNSUPPORTED;
+}
+
+__global__ void nmg_zero_kernel(void* C, int64_t M, int64_t N, int64_t ldc, int esz) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= M * N) return;
+    const int64_t r = i / N, c = i - r * N;
+    if (esz == 4) static_cast<float*>(C)[r * ldc + c] = 0.0f;
+    else static_cast<uint16_t*>(C)[r * ldc + c] = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+sten_status sten_nmg_sparsify(sten_nmg f, sten_dtype dt, const void* W, int64_t M, int64_t K, int64_t ldw,
+                              void* values, uint16_t* idx, void* stream) {
+    NmgArgs a = {};
+    sten_status s = nmg_setup(f, dt, M, K, &a);
+    if (s) return s;
+    if (ldw < K) return STEN_ERR_SHAPE;
+    if (M * K > 0 && (!W || !values || !idx)) return STEN_ERR_INVALID_ARG;
+    if (M == 0 || K == 0) return STEN_OK;
+    a.W = W; a.ldw = ldw; a.values = values; a.idx = idx;
+    const int64_t chunks = a.RB * a.NC;
+    const size_t smem = size_t(kNmgWarpsPerCta) * nmg_warp_smem(a.L, a.C);
+    const unsigned grid = unsigned((chunks + kNmgWarpsPerCta - 1) / kNmgWarpsPerCta);
+    cudaStream_t st = nmg_stream(stream);
+    if (dt == STEN_F32) {
+        if (cudaFuncSetAttribute(nmg_sparsify_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))
+            return STEN_ERR_CUDA;
+        nmg_sparsify_kernel<float><<<grid, kNmgWarpsPerCta * 32, smem, st>>>(a);
+    } else {
+        if (cudaFuncSetAttribute(nmg_sparsify_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem)))
+            return STEN_ERR_CUDA;
+        nmg_sparsify_kernel<uint16_t><<<grid, kNmgWarpsPerCta * 32, smem, st>>>(a);
+    }
+    return nmg_last_cuda();
+}
+
+sten_status sten_nmg_densify(sten_nmg f, sten_dtype dt, const void* values, const uint16_t* idx, int64_t M,
+                             int64_t K, void* W_out, int64_t ldw, void* stream) {
+    NmgArgs a = {};
+    sten_status s = nmg_setup(f, dt, M, K, &a);
+    if (s) return s;
+    if (ldw < K) return STEN_ERR_SHAPE;
+    if (M * K > 0 && (!W_out || !values || !idx)) return STEN_ERR_INVALID_ARG;
+    if (M == 0 || K == 0) return STEN_OK;
+    a.values_in = values; a.idx_in = idx; a.ldw = ldw;
+    const int64_t threads = a.RB * a.NC * a.L;
+    const unsigned grid = unsigned((threads + 255) / 256);
+    cudaStream_t st = nmg_stream(stream);
+    if (dt == STEN_F32) nmg_densify_kernel<float><<<grid, 256, 0, st>>>(a, static_cast<float*>(W_out));
+    else nmg_densify_kernel<uint16_t><<<grid, 256, 0, st>>>(a, static_cast<uint16_t*>(W_out));
+    return nmg_last_cuda();
+}
+
+sten_status sten_nmg_spmm(sten_nmg f, sten_dtype ab_dt, const void* values, const uint16_t* idx, int64_t M,
+                          int64_t K, const void* B, int64_t ldb, int64_t N, void* C, int64_t ldc,
+                          sten_dtype c_dt, void* stream) {
+    NmgArgs fa = {};
+    sten_status s = nmg_setup(f, ab_dt, M, K, &fa);
+    if (s) return s;
+    if (!nmg_dtype_ok(c_dt)) return STEN_ERR_INVALID_ARG;
+    if (N < 0 || ldb < N || ldc < N) return STEN_ERR_SHAPE;
+    if ((M * K > 0 && (!values || !idx)) || (K * N > 0 && !B) || (M * N > 0 && !C)) return STEN_ERR_INVALID_ARG;
+    const bool compiled = (f.n == 1 && (f.m == 2 || f.m == 4 || f.m == 8)) || (f.n == 2 && f.m == 4);
+    if (!compiled) return STEN_ERR_UNSUPPORTED;
+    const size_t sab = nmg_dt_size(ab_dt);
+    if (K * N > 0 && ((reinterpret_cast<uintptr_t>(B) & 15u) != 0 || (ldb * int64_t(sab)) % 16 != 0))
+        return STEN_ERR_UNSUPPORTED;
+    if (M == 0 || N == 0) return STEN_OK;
+    cudaStream_t st = nmg_stream(stream);
+    if (K == 0) {
+        nmg_zero_kernel<<<unsigned((M * N + 255) / 256), 256, 0, st>>>(C, M, N, ldc, int(nmg_dt_size(c_dt)));
+        return nmg_last_cuda();
+    }
+    NmgSpmmArgs a = {};
+    a.values = values; a.idx = idx; a.B = B; a.C = C;
+    a.M = M; a.K = K; a.N = N; a.ldb = ldb; a.ldc = ldc; a.NC = fa.NC; a.RB = fa.RB;
+    a.g = f.g; a.L = fa.L;
+    if (ab_dt == STEN_F32)
+        return c_dt == STEN_F32 ? dispatch_nmg_spmm<float, float>(f.n, f.m, a, st)
+                                : dispatch_nmg_spmm<float, uint16_t>(f.n, f.m, a, st);
+    return c_dt == STEN_F32 ? dispatch_nmg_spmm<uint16_t, float>(f.n, f.m, a, st)
+                            : dispatch_nmg_spmm<uint16_t, uint16_t>(f.n, f.m, a, st);
+}
+
+}  // extern "C"

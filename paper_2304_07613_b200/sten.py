@@ -8,6 +8,7 @@ missing, the calls raise.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 
 import torch
@@ -59,6 +60,10 @@ SIGNATURES = {
                                                                 ctypes.c_int]),
     "sten_sparse_linear_host": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _i64, _i64,
                                                _vp, _i64, ctypes.c_int, _vp, _i64, _vp]),
+    "sten_nmg_sparsify": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "sten_nmg_densify": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
+    "sten_nmg_spmm": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64, _i64,
+                                     _vp, _i64, ctypes.c_int, _vp]),
     "sten_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "sten_algo_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "sten_spmm_launch_count": (ctypes.c_int32, [ctypes.POINTER(sten_spmm_plan)]),
@@ -232,3 +237,50 @@ def algo_name(algo: int) -> str:
 
 def status_string(s: int) -> str:
     return load().sten_status_string(s).decode()
+
+
+# ---------------------------------------------------------------------------------------------
+# Chunked n:m:g -- the paper's own format (include/sten.h "Chunked n:m:g")
+# ---------------------------------------------------------------------------------------------
+def nmg_chunk(n: int, m: int, g: int) -> int:
+    """L = C(m, n) g columns per chunk."""
+    return math.comb(m, n) * g
+
+
+def nmg_sparsify(W: torch.Tensor, n: int, m: int, g: int, values: torch.Tensor | None = None,
+                 idx: torch.Tensor | None = None, stream=None):
+    """dense W [M][K] -> (values [M/m][K/L][L][n], idx [M/m][K/L][L] int16 bit patterns of uint16)."""
+    _cuda(W, "W")
+    M, K = W.shape
+    L = nmg_chunk(n, m, g)
+    if values is None:
+        values = torch.empty((M // m, K // L, L, n), dtype=W.dtype, device=W.device)
+    if idx is None:
+        idx = torch.empty((M // m, K // L, L), dtype=torch.int16, device=W.device)
+    _check(load().sten_nmg_sparsify(sten_nmg(n, m, g), _dt(W), W.data_ptr(), M, K, _ld(W),
+                                    values.data_ptr(), idx.data_ptr(), _stream(stream)), "sten_nmg_sparsify")
+    return values, idx
+
+
+def nmg_densify(values: torch.Tensor, idx: torch.Tensor, n: int, m: int, g: int, K: int,
+                out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    M = values.shape[0] * m
+    if out is None:
+        out = torch.empty((M, K), dtype=values.dtype, device=values.device)
+    _check(load().sten_nmg_densify(sten_nmg(n, m, g), _dt(values), values.data_ptr(), idx.data_ptr(), M, K,
+                                   out.data_ptr(), _ld(out), _stream(stream)), "sten_nmg_densify")
+    return out
+
+
+def nmg_spmm(values: torch.Tensor, idx: torch.Tensor, B: torch.Tensor, n: int, m: int, g: int,
+             out: torch.Tensor | None = None, out_dtype=None, stream=None) -> torch.Tensor:
+    """C [M][N] = densify(values, idx) @ B [K][N] (chunked n:m:g)."""
+    _cuda(B, "B")
+    M = values.shape[0] * m
+    K, N = B.shape
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype or values.dtype, device=B.device)
+    _check(load().sten_nmg_spmm(sten_nmg(n, m, g), _dt(values), values.data_ptr(), idx.data_ptr(), M, K,
+                                B.data_ptr(), _ld(B), N, out.data_ptr(), _ld(out), _dt(out), _stream(stream)),
+           "sten_nmg_spmm")
+    return out
