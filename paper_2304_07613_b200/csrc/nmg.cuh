@@ -72,9 +72,12 @@ struct NmgArgs {
 // largest still-acceptable item (acceptability only ever turns false), which is what each
 // step's warp-wide max does.
 constexpr int kNmgWarpsPerCta = 4;
+constexpr int kNmgRegKeys = 8;          // keys per lane held in registers when L C <= 256
 
-__host__ __device__ inline size_t nmg_warp_smem(int L, int C) {
-    return (size_t(L) * C * 8 + size_t(L) * 2 + size_t(C) * 4 + 15) & ~size_t(15);
+__host__ __device__ inline size_t nmg_warp_smem(int L, int C, int m, int esz) {
+    const size_t keys = size_t(L) * C * 8;
+    const size_t w = (size_t(m) * L * esz + 15) & ~size_t(15);
+    return keys + w + ((size_t(C) * 4 + size_t(L) * 2 + 15) & ~size_t(15));
 }
 
 template <typename T>
@@ -85,47 +88,79 @@ nmg_sparsify_kernel(const NmgArgs a) {
     const int64_t chunk = int64_t(blockIdx.x) * kNmgWarpsPerCta + warp;
     if (chunk >= a.RB * a.NC) return;
     const int64_t rb = chunk / a.NC, c = chunk - rb * a.NC;
-    const int L = a.L, C = a.C, n = a.n, g = a.g;
-    unsigned char* ws = smem + size_t(warp) * nmg_warp_smem(L, C);
+    const int L = a.L, C = a.C, n = a.n, g = a.g, m = a.m;
+    unsigned char* ws = smem + size_t(warp) * nmg_warp_smem(L, C, m, int(sizeof(T)));
     unsigned long long* key = reinterpret_cast<unsigned long long*>(ws);
-    int* cnt = reinterpret_cast<int*>(ws + size_t(L) * C * 8);                       // 4-byte aligned
-    int16_t* pat_of = reinterpret_cast<int16_t*>(ws + size_t(L) * C * 8 + size_t(C) * 4);
+    T* sw = reinterpret_cast<T*>(ws + size_t(L) * C * 8);                       // the m x L block of W
+    unsigned char* tail = ws + size_t(L) * C * 8 + ((size_t(m) * L * sizeof(T) + 15) & ~size_t(15));
+    int* cnt = reinterpret_cast<int*>(tail);                                     // 4-byte aligned
+    int16_t* pat_of = reinterpret_cast<int16_t*>(tail + size_t(C) * 4);
     const T* W = static_cast<const T*>(a.W);
     const T* w0 = W + rb * a.m * a.ldw + c * L;   // column b, row r: w0[r * ldw + b]
 
-    const int NI = L * C;
-    for (int i = lane; i < NI; i += 32) {
-        const int b = i / C, p = i - b * C;
-        const uint32_t mk = a.pat.mask[p];
-        float s = 0.0f;
-        for (int t = 0; t < n; ++t) s = __fadd_rn(s, fabsf(to_f32(w0[int64_t(nmg_pos(mk, t)) * a.ldw + b])));
-        key[i] = (static_cast<unsigned long long>(__float_as_uint(s)) << 32) |
-                 (static_cast<unsigned long long>(0xFFFFu - uint32_t(b)) << 16) | (0xFFFFu - uint32_t(p));
+    // the chunk's m x L block, row by row (coalesced), into shared memory
+    for (int e = lane; e < m * L; e += 32) {
+        const int r = e / L, b = e - r * L;
+        sw[e] = w0[int64_t(r) * a.ldw + b];
     }
     for (int b = lane; b < L; b += 32) pat_of[b] = -1;
     for (int p = lane; p < C; p += 32) cnt[p] = 0;
     __syncwarp();
-    for (int step = 0; step < L; ++step) {
-        unsigned long long best = 0ull;
-        for (int i = lane; i < NI; i += 32) {
-            const unsigned long long k = key[i];
-            const int b = int(0xFFFFu - uint32_t((k >> 16) & 0xFFFFu));
-            const int p = int(0xFFFFu - uint32_t(k & 0xFFFFu));
-            if (k > best && pat_of[b] < 0 && cnt[p] < g) best = k;
-        }
+    const int NI = L * C;
+    auto make_key = [&](int i) -> unsigned long long {
+        const int b = i / C, p = i - b * C;
+        const uint32_t mk = a.pat.mask[p];
+        float s = 0.0f;
+        for (int t = 0; t < n; ++t) s = __fadd_rn(s, fabsf(to_f32(sw[nmg_pos(mk, t) * L + b])));
+        return (static_cast<unsigned long long>(__float_as_uint(s)) << 32) |
+               (static_cast<unsigned long long>(0xFFFFu - uint32_t(b)) << 16) | (0xFFFFu - uint32_t(p));
+    };
+    // warp max of a 64-bit key with two redux.sync: max of the high words, then max of the low
+    // words among the lanes holding that high word
+    auto warp_max = [&](unsigned long long k) {
+        const uint32_t hi = uint32_t(k >> 32), lo = uint32_t(k);
+        const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+        const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+        return (static_cast<unsigned long long>(mh) << 32) | ml;
+    };
+    auto kb = [](unsigned long long k) { return int(0xFFFFu - uint32_t((k >> 16) & 0xFFFFu)); };
+    auto kp = [](unsigned long long k) { return int(0xFFFFu - uint32_t(k & 0xFFFFu)); };
+
+    if (NI <= 32 * kNmgRegKeys) {
+        // keys in registers; a key is zeroed when its column is taken or its pattern is full
+        unsigned long long kr[kNmgRegKeys];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
-            best = other > best ? other : best;
+        for (int j = 0; j < kNmgRegKeys; ++j) kr[j] = lane + 32 * j < NI ? make_key(lane + 32 * j) : 0ull;
+        for (int step = 0; step < L; ++step) {
+            unsigned long long best = 0ull;
+#pragma unroll
+            for (int j = 0; j < kNmgRegKeys; ++j) best = kr[j] > best ? kr[j] : best;
+            best = warp_max(best);
+            const int b = kb(best), p = kp(best);
+            const int c_old = cnt[p];
+            __syncwarp();
+            if (lane == 0) { pat_of[b] = int16_t(p); cnt[p] = c_old + 1; }
+            __syncwarp();
+            const bool full = c_old + 1 >= g;
+#pragma unroll
+            for (int j = 0; j < kNmgRegKeys; ++j)
+                if (kr[j] != 0ull && (kb(kr[j]) == b || (full && kp(kr[j]) == p))) kr[j] = 0ull;
         }
-        if (lane == 0) {
-            const int b = int(0xFFFFu - uint32_t((best >> 16) & 0xFFFFu));
-            const int p = int(0xFFFFu - uint32_t(best & 0xFFFFu));
-            pat_of[b] = int16_t(p);
-            cnt[p] += 1;
-        }
+    } else {
+        for (int i = lane; i < NI; i += 32) key[i] = make_key(i);
         __syncwarp();
+        for (int step = 0; step < L; ++step) {
+            unsigned long long best = 0ull;
+            for (int i = lane; i < NI; i += 32) {
+                const unsigned long long k = key[i];
+                if (k > best && pat_of[kb(k)] < 0 && cnt[kp(k)] < g) best = k;
+            }
+            best = warp_max(best);
+            if (lane == 0) { pat_of[kb(best)] = int16_t(kp(best)); cnt[kp(best)] += 1; }
+            __syncwarp();
+        }
     }
+    __syncwarp();
     // store: slot = p g + (number of lower columns with the same pattern)
     T* V = static_cast<T*>(a.values);
     const int64_t base = chunk * L;
@@ -136,7 +171,7 @@ nmg_sparsify_kernel(const NmgArgs a) {
         const int64_t slot = base + int64_t(p) * g + rank;
         a.idx[slot] = uint16_t(b);
         const uint32_t mk = a.pat.mask[p];
-        for (int t = 0; t < n; ++t) V[slot * n + t] = w0[int64_t(nmg_pos(mk, t)) * a.ldw + b];
+        for (int t = 0; t < n; ++t) V[slot * n + t] = sw[nmg_pos(mk, t) * L + b];
     }
 }
 
@@ -161,15 +196,17 @@ __global__ void __launch_bounds__(256) nmg_densify_kernel(const NmgArgs a, T* __
 }
 
 // ---- product (Fig. 5) ----------------------------------------------------------------------------
-// CTA = 8 warps x BN = 128 tokens (lane: 4 consecutive tokens); warp w owns RBW row blocks (m
-// rows each; accumulators acc[RBW][m][4] in registers, static row indices because the pattern
-// order is a compile-time table -- the paper's "chunks, which fix the order of sparsity
-// permutations, allow kernels to avoid branches based on the sparsity structure").
-// A K-stage of CPS whole chunks (CPS L rows of B) is staged in shared memory by cp.async (double
-// buffered) and shared by every row block of the CTA; per slot a warp reads the idx and the n
-// values (uniform loads, L1 broadcast), gathers its B row from shared memory (LDS.128 for fp32)
-// and does 4 n FMAs per lane -- "broadcast into vector registers ... indirect loads from specific
-// rows of B ... FMA".
+// CTA = 16 warps x BN = 128 tokens (lane: 4 consecutive tokens); warp w owns row block rb0 + w (m
+// rows; accumulators acc[m][4] in registers with static row indices, because the pattern order
+// is a compile-time table -- "chunks, which fix the order of sparsity permutations, allow kernels
+// to avoid branches based on the sparsity structure").  A K-stage of CPS whole
+// chunks is staged in shared memory by cp.async (double buffered): the CPS L rows of B (shared by
+// the CTA's 16 row blocks) and, per row block, its CPS L idx entries and CPS L n values.  Per slot
+// a warp reads the idx (broadcast), gathers its B row (LDS.128 for fp32), reads the n values
+// (broadcast) and does 4 n FMAs per lane -- "loaded from sparse values, then broadcast into vector
+// registers ... indirect loads from specific rows of B ... FMA".  Each gathered
+// B element feeds n FMAs (the (A) layout's gathered element feeds g), so for fp32 the shared-memory
+// datapath caps this kernel at ~n/4 of the FFMA peak.
 struct NmgSpmmArgs {
     const void* values;
     const uint16_t* idx;
@@ -179,120 +216,144 @@ struct NmgSpmmArgs {
     int g, L, cps;          // cps = chunks per K-stage
 };
 
-constexpr int kNmgSpmmWarps = 8;
+constexpr int kNmgSpmmWarps = 16;
+constexpr int kNmgStages = 3;
 constexpr int kNmgBN = 128;
 
+// per-stage shared memory: B [cps L][BN] | idx [8][cps L] u16 | values [8][cps L n]
 template <typename TAB>
-__host__ __device__ inline size_t nmg_spmm_stage_bytes(int rows) {
-    return size_t(rows) * kNmgBN * sizeof(TAB);
+__host__ __device__ inline size_t nmg_spmm_stage_bytes(int rows, int n) {
+    const size_t b = size_t(rows) * kNmgBN * sizeof(TAB);
+    const size_t i = (size_t(kNmgSpmmWarps) * rows * 2 + 15) & ~size_t(15);
+    const size_t v = (size_t(kNmgSpmmWarps) * rows * n * sizeof(TAB) + 15) & ~size_t(15);
+    return b + i + v;
 }
 
-template <typename TAB, typename TC, int NN, int MM, int RBW>
+template <typename TAB, typename TC, int NN, int MM>
 __global__ void __launch_bounds__(kNmgSpmmWarps * 32)
 nmg_spmm_kernel(const NmgSpmmArgs a) {
     constexpr NmgPatterns P = nmg_revolving_door(MM, NN);
     constexpr int CP = nmg_binom(MM, NN);
     static_assert(CP <= kNmgMaxPatterns, "too many patterns");
     constexpr int EV = 4;                                   // tokens per lane
+    constexpr int NT = kNmgSpmmWarps * 32;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t n0 = int64_t(blockIdx.x) * kNmgBN;
-    const int64_t rb0 = (int64_t(blockIdx.y) * kNmgSpmmWarps + warp) * RBW;
+    const int64_t rbc = int64_t(blockIdx.y) * kNmgSpmmWarps;          // first row block of the CTA
     const int L = a.L, g = a.g;
-    const int rows = a.cps * L;                             // B rows per stage
-    const size_t stage_bytes = nmg_spmm_stage_bytes<TAB>(rows);
+    const int rows = a.cps * L;                                        // B rows per stage
+    const size_t b_bytes = size_t(rows) * kNmgBN * sizeof(TAB);
+    const size_t i_bytes = (size_t(kNmgSpmmWarps) * rows * 2 + 15) & ~size_t(15);
+    const size_t stage_bytes = nmg_spmm_stage_bytes<TAB>(rows, NN);
     const TAB* B = static_cast<const TAB*>(a.B);
+    const TAB* V = static_cast<const TAB*>(a.values);
     const int64_t nstages = (a.NC + a.cps - 1) / a.cps;
 
-    // cooperative cp.async of one stage: rows [c0 L, (c0 + cps) L) x tokens [n0, n0 + BN)
-    constexpr int CH = kNmgBN * int(sizeof(TAB)) / 16;      // 16-byte chunks per staged row
     auto load_stage = [&](int64_t st, int buf) {
         unsigned char* dst = smem + size_t(buf) * stage_bytes;
-        const int64_t k0 = st * a.cps * L;
-        for (int e = threadIdx.x; e < rows * CH; e += kNmgSpmmWarps * 32) {
+        const int64_t c0 = st * a.cps;
+        const int nch = int(min64(a.cps, a.NC - c0));
+        const int64_t k0 = c0 * L;
+        constexpr int CH = kNmgBN * int(sizeof(TAB)) / 16;            // 16-byte chunks per B row
+        for (int e = threadIdx.x; e < rows * CH; e += NT) {
             const int r = e / CH, ch = e - r * CH;
             const int64_t k = k0 + r;
             const int64_t col = n0 + int64_t(ch) * (16 / int(sizeof(TAB)));
             int bytes = 0;
-            if (k < a.K && col < a.N) bytes = int(min64(16, (a.N - col) * int64_t(sizeof(TAB))));
+            if (r < nch * L && col < a.N) bytes = int(min64(16, (a.N - col) * int64_t(sizeof(TAB))));
             cp_async16(dst + size_t(r) * kNmgBN * sizeof(TAB) + size_t(ch) * 16, bytes ? B + k * a.ldb + col : B,
                        bytes);
+        }
+        // idx and values of the CTA's row blocks: contiguous runs (4-byte words; L is even for
+        // every compiled format, so runs start and end on 4-byte boundaries)
+        const int iw = nch * L / 2, vw = nch * L * NN * int(sizeof(TAB)) / 4;
+        for (int e = threadIdx.x; e < kNmgSpmmWarps * (iw + vw); e += NT) {
+            const int w = e / (iw + vw), o = e - w * (iw + vw);
+            const int64_t rb = rbc + w;
+            const bool ok = rb < a.RB;
+            const int64_t chunk = ok ? rb * a.NC + c0 : 0;
+            if (o < iw) {
+                cp_async4(dst + b_bytes + (size_t(w) * rows) * 2 + size_t(o) * 4,
+                          reinterpret_cast<const unsigned char*>(a.idx + chunk * L) + size_t(o) * 4, ok ? 4 : 0);
+            } else {
+                const int ov = o - iw;
+                cp_async4(dst + b_bytes + i_bytes + size_t(w) * rows * NN * sizeof(TAB) + size_t(ov) * 4,
+                          reinterpret_cast<const unsigned char*>(V + chunk * L * NN) + size_t(ov) * 4, ok ? 4 : 0);
+            }
         }
         cp_async_commit();
     };
 
-    float acc[RBW][MM][EV];
+    float acc[MM][EV];
 #pragma unroll
-    for (int q = 0; q < RBW; ++q)
+    for (int r = 0; r < MM; ++r)
 #pragma unroll
-        for (int r = 0; r < MM; ++r)
-#pragma unroll
-            for (int e = 0; e < EV; ++e) acc[q][r][e] = 0.0f;
+        for (int e = 0; e < EV; ++e) acc[r][e] = 0.0f;
 
-    const TAB* V = static_cast<const TAB*>(a.values);
-    if (nstages > 0) load_stage(0, 0);
+    const int64_t rb = rbc + warp;
+    // kNmgStages-deep ring: stages st+1 .. st+kNmgStages-1 are in flight while st is consumed
+    for (int64_t st = 0; st < kNmgStages - 1; ++st) {
+        if (st < nstages) load_stage(st, int(st));
+        else cp_async_commit();                                        // keep the group count uniform
+    }
     for (int64_t st = 0; st < nstages; ++st) {
-        const int buf = int(st & 1);
-        if (st + 1 < nstages) {
-            load_stage(st + 1, buf ^ 1);
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        }
-        __syncthreads();
-        const unsigned char* sB = smem + size_t(buf) * stage_bytes + size_t(lane) * EV * sizeof(TAB);
-        const int64_t c_begin = st * a.cps;
-        const int nch = int(min64(a.cps, a.NC - c_begin));
-#pragma unroll
-        for (int q = 0; q < RBW; ++q) {
-            const int64_t rb = rb0 + q;
-            if (rb >= a.RB) break;
+        const int buf = int(st % kNmgStages);
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kNmgStages - 2) : "memory");
+        __syncthreads();                                               // stage st visible; st-1 consumed
+        if (st + kNmgStages - 1 < nstages) load_stage(st + kNmgStages - 1, int((st + kNmgStages - 1) % kNmgStages));
+        else cp_async_commit();
+        if (rb < a.RB) {
+            const unsigned char* sb = smem + size_t(buf) * stage_bytes;
+            const uint32_t sB = smem_u32(sb) + uint32_t(lane) * EV * uint32_t(sizeof(TAB));
+            const uint16_t* sI = reinterpret_cast<const uint16_t*>(sb + b_bytes) + size_t(warp) * rows;
+            const TAB* sV = reinterpret_cast<const TAB*>(sb + b_bytes + i_bytes) + size_t(warp) * rows * NN;
+            const int nch = int(min64(a.cps, a.NC - st * a.cps));
             for (int cl = 0; cl < nch; ++cl) {
-                const int64_t chunk = rb * a.NC + c_begin + cl;
-                const uint16_t* ip = a.idx + chunk * L;
-                const TAB* vp = V + chunk * L * NN;
-                const unsigned char* sc = sB + size_t(cl) * L * kNmgBN * sizeof(TAB);
+                const uint32_t sBc = sB + uint32_t(cl * L) * kNmgBN * uint32_t(sizeof(TAB));
+                const uint16_t* ip = sI + cl * L;
+                const TAB* vp = sV + size_t(cl) * L * NN;
 #pragma unroll
                 for (int p = 0; p < CP; ++p) {
+#pragma unroll 4
                     for (int j = 0; j < g; ++j) {
                         const int s = p * g + j;
-                        const int b = __ldg(ip + s);
-                        float bv[EV];
+                        const uint32_t addr = sBc + uint32_t(ip[s]) * kNmgBN * uint32_t(sizeof(TAB));
+                        float2 b01, b23;
                         if constexpr (sizeof(TAB) == 4) {
-                            const float4 t4 = *reinterpret_cast<const float4*>(sc + size_t(b) * kNmgBN * 4);
-                            bv[0] = t4.x; bv[1] = t4.y; bv[2] = t4.z; bv[3] = t4.w;
+                            const float4 t4 = lds128_addr(addr);
+                            b01 = make_float2(t4.x, t4.y);
+                            b23 = make_float2(t4.z, t4.w);
                         } else {
-                            const uint2 t2 = *reinterpret_cast<const uint2*>(sc + size_t(b) * kNmgBN * 2);
-                            bv[0] = __uint_as_float(t2.x << 16); bv[1] = __uint_as_float(t2.x & 0xffff0000u);
-                            bv[2] = __uint_as_float(t2.y << 16); bv[3] = __uint_as_float(t2.y & 0xffff0000u);
+                            uint32_t w0, w1;
+                            asm("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(w0), "=r"(w1) : "r"(addr));
+                            b01 = make_float2(__uint_as_float(w0 << 16), __uint_as_float(w0 & 0xffff0000u));
+                            b23 = make_float2(__uint_as_float(w1 << 16), __uint_as_float(w1 & 0xffff0000u));
                         }
 #pragma unroll
                         for (int t = 0; t < NN; ++t) {
                             const float v = to_f32(vp[s * NN + t]);
                             const int r = nmg_pos(P.mask[p], t);
-#pragma unroll
-                            for (int e = 0; e < EV; ++e) acc[q][r][e] = fmaf(v, bv[e], acc[q][r][e]);
+                            float2& c01 = *reinterpret_cast<float2*>(&acc[r][0]);
+                            float2& c23 = *reinterpret_cast<float2*>(&acc[r][2]);
+                            c01 = __ffma2_rn(make_float2(v, v), b01, c01);
+                            c23 = __ffma2_rn(make_float2(v, v), b23, c23);
                         }
                     }
                 }
             }
         }
-        __syncthreads();                                    // buffer buf is refilled next stage
     }
+    if (rb >= a.RB) return;
     // epilogue: rows rb m + r, tokens n0 + 4 lane + e
     TC* Cp = static_cast<TC*>(a.C);
 #pragma unroll
-    for (int q = 0; q < RBW; ++q) {
-        const int64_t rb = rb0 + q;
-        if (rb >= a.RB) break;
+    for (int r = 0; r < MM; ++r) {
+        TC* row = Cp + (rb * MM + r) * a.ldc;
 #pragma unroll
-        for (int r = 0; r < MM; ++r) {
-            TC* row = Cp + (rb * MM + r) * a.ldc;
-#pragma unroll
-            for (int e = 0; e < EV; ++e) {
-                const int64_t col = n0 + int64_t(lane) * EV + e;
-                if (col < a.N) row[col] = from_f32<TC>(acc[q][r][e]);
-            }
+        for (int e = 0; e < EV; ++e) {
+            const int64_t col = n0 + int64_t(lane) * EV + e;
+            if (col < a.N) row[col] = from_f32<TC>(acc[r][e]);
         }
     }
 }

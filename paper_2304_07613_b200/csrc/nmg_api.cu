@@ -33,17 +33,16 @@ sten_status nmg_setup(sten_nmg f, int dt, int64_t M, int64_t K, NmgArgs* a) {
 
 template <typename TAB, typename TC, int NN, int MM>
 sten_status launch_nmg_spmm(const NmgSpmmArgs& a0, cudaStream_t st) {
-    constexpr int RBW = MM <= 4 ? 2 : 1;
     NmgSpmmArgs a = a0;
     a.cps = a.L >= 64 ? 1 : (64 + a.L - 1) / a.L;                   // >= 64 B rows per K-stage
     if (a.cps > a.NC) a.cps = int(a.NC > 0 ? a.NC : 1);
-    const size_t smem = 2 * nmg_spmm_stage_bytes<TAB>(a.cps * a.L);
+    while (a.cps > 1 && kNmgStages * nmg_spmm_stage_bytes<TAB>(a.cps * a.L, NN) > 227 * 1024) --a.cps;
+    const size_t smem = kNmgStages * nmg_spmm_stage_bytes<TAB>(a.cps * a.L, NN);
     if (smem > 227 * 1024) return STEN_ERR_UNSUPPORTED;
-    auto kern = nmg_spmm_kernel<TAB, TC, NN, MM, RBW>;
+    auto kern = nmg_spmm_kernel<TAB, TC, NN, MM>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
         return STEN_ERR_CUDA;
-    const int64_t rb_per_cta = int64_t(kNmgSpmmWarps) * RBW;
-    dim3 grid(unsigned((a.N + kNmgBN - 1) / kNmgBN), unsigned((a.RB + rb_per_cta - 1) / rb_per_cta));
+    dim3 grid(unsigned((a.N + kNmgBN - 1) / kNmgBN), unsigned((a.RB + kNmgSpmmWarps - 1) / kNmgSpmmWarps));
     kern<<<grid, kNmgSpmmWarps * 32, smem, st>>>(a);
     return nmg_last_cuda();
 }
@@ -79,7 +78,7 @@ sten_status sten_nmg_sparsify(sten_nmg f, sten_dtype dt, const void* W, int64_t 
     if (M == 0 || K == 0) return STEN_OK;
     a.W = W; a.ldw = ldw; a.values = values; a.idx = idx;
     const int64_t chunks = a.RB * a.NC;
-    const size_t smem = size_t(kNmgWarpsPerCta) * nmg_warp_smem(a.L, a.C);
+    const size_t smem = size_t(kNmgWarpsPerCta) * nmg_warp_smem(a.L, a.C, a.m, int(nmg_dt_size(dt)));
     const unsigned grid = unsigned((chunks + kNmgWarpsPerCta - 1) / kNmgWarpsPerCta);
     cudaStream_t st = nmg_stream(stream);
     if (dt == STEN_F32) {
@@ -123,6 +122,9 @@ sten_status sten_nmg_spmm(sten_nmg f, sten_dtype ab_dt, const void* values, cons
     if ((M * K > 0 && (!values || !idx)) || (K * N > 0 && !B) || (M * N > 0 && !C)) return STEN_ERR_INVALID_ARG;
     const bool compiled = (f.n == 1 && (f.m == 2 || f.m == 4 || f.m == 8)) || (f.n == 2 && f.m == 4);
     if (!compiled) return STEN_ERR_UNSUPPORTED;
+    // idx / values are staged with 4-byte cp.async (L is even for every compiled format)
+    if ((reinterpret_cast<uintptr_t>(idx) & 3u) != 0 || (reinterpret_cast<uintptr_t>(values) & 3u) != 0)
+        return STEN_ERR_UNSUPPORTED;
     const size_t sab = nmg_dt_size(ab_dt);
     if (K * N > 0 && ((reinterpret_cast<uintptr_t>(B) & 15u) != 0 || (ldb * int64_t(sab)) % 16 != 0))
         return STEN_ERR_UNSUPPORTED;
