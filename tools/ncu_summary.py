@@ -64,10 +64,19 @@ def launches(tag):
     return path, rows
 
 
+def have_full(tag, suffix):
+    return any(os.path.exists(os.path.join(OUT, tag + suffix + e)) for e in (".ncu-rep", "_raw.csv"))
+
+
 def full(tag, suffix="_full"):
     rep = os.path.join(OUT, tag + suffix + ".ncu-rep")
-    raw = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], text=True)
-    rows = list(csv.reader(raw.splitlines()))
+    raw_csv = os.path.join(OUT, tag + suffix + "_raw.csv")
+    if os.path.exists(rep):
+        raw = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], text=True)
+    else:                               # exported on the box by tools/profile.sh
+        with open(raw_csv) as fh:
+            raw = fh.read()
+    rows = list(csv.reader([l for l in raw.splitlines() if l.startswith('"')]))
     hdr = rows[0]
     d = dict(zip(hdr, rows[2]))
     out = {"kernel": d.get("Kernel Name"), "grid": d.get("Grid Size"), "block": d.get("Block Size")}
@@ -107,10 +116,20 @@ def main():
                        "launches): compare shares, not absolute times")
     rep, f = full(a.tag)
     summary["dominant_launch_full_set"] = f
-    if os.path.exists(os.path.join(OUT, a.tag + "_tc_full.ncu-rep")):
+    if have_full(a.tag, "_tc_full"):
         _, ftc = full(a.tag, "_tc_full")
         ftc["note"] = "C3 1024x4096x16384 1:4 g=64 bf16, tcgen05 kernel (K5), first launch"
         summary["tcgen05_launch_full_set"] = ftc
+    if have_full(a.tag, "_sp_full"):
+        _, fsp = full(a.tag, "_sp_full")
+        fsp["note"] = "K1 sparsify of the dominant case (768x3072 2:4 g=4 fp32)"
+        summary["sparsify_launch_full_set"] = fsp
+    # the exported CSVs of the full captures travel into profiles/ (raw metrics + details page)
+    for suffix, name in (("_full", "dominant"), ("_tc_full", "tcgen05"), ("_sp_full", "sparsify")):
+        for page in ("raw", "details"):
+            src = os.path.join(OUT, "%s%s_%s.csv" % (a.tag, suffix, page))
+            if os.path.exists(src):
+                shutil.copy(src, os.path.join(PROF, "ncu_r%s_%s_%s.csv" % (a.round, name, page)))
     with open(os.path.join(PROF, "ncu_r%s_summary.json" % a.round), "w") as fh:
         json.dump(summary, fh, indent=1)
     spmm = [v for k, v in summary["launch_list"].items() if k.startswith("spmm")]

@@ -27,3 +27,20 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm
    python bench.py --config 2 --g 64 --profile --steps 1 --warmup 1 --no-graph --lanes 1 --no-tune \
    > gpurun_out/${tag}_ncu_tc_full.log 2>&1
 echo "ncu tc full rc=$?"
+# 5. one `ncu --set full` capture of the K1 sparsify launch of the dominant case
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sparsify -s ${DOM} -c 1 -o gpurun_out/${tag}_sp_full \
+   python bench.py --profile --steps 1 --warmup 1 --no-graph --lanes 1 --plans-in gpurun_out/${tag}_plans.json "$@" \
+   > gpurun_out/${tag}_ncu_sp_full.log 2>&1
+echo "ncu sparsify full rc=$?"
+# export the full captures to CSV (raw metrics, details, per-instruction source) and drop the
+# .ncu-rep files so gpurun_out/ stays under the 64 MiB copy-back limit
+for r in full tc_full sp_full; do
+  f=gpurun_out/${tag}_${r}.ncu-rep
+  if [ -f $f ]; then
+    ncu -i $f --page raw --csv > gpurun_out/${tag}_${r}_raw.csv 2>/dev/null
+    ncu -i $f --page details --csv > gpurun_out/${tag}_${r}_details.csv 2>/dev/null
+    ncu -i $f --page source --csv --print-source sass > gpurun_out/${tag}_${r}_source.csv 2>/dev/null
+    rm -f $f
+  fi
+done
+ls -la gpurun_out/
