@@ -205,6 +205,16 @@ sten_status sten_nmg_spmm(sten_nmg f, sten_dtype ab_dt,
                           const void* B, int64_t ldb, int64_t N,
                           void* C, int64_t ldc, sten_dtype c_dt, void* stream);
 
+/* sten_sparse_linear_host without the final wait: the copies and kernels are only enqueued
+ * on `stream` (host buffers must be pinned and stay valid, and C_host is written, when the
+ * stream reaches the D2H copy); the caller synchronises.  Calls on different streams overlap
+ * their PCIe copies with each other's kernels. */
+sten_status sten_sparse_linear_host_async(sten_nmg f, sten_dtype ab_dt,
+                                          const void* W_host, int64_t M, int64_t K, int64_t ldw,
+                                          const void* B_host, int64_t ldb, int64_t N,
+                                          void* C_host, int64_t ldc, sten_dtype c_dt,
+                                          void* workspace, int64_t workspace_bytes, void* stream);
+
 const char* sten_status_string(sten_status s);
 const char* sten_algo_name(int32_t algo);
 /* Number of kernel launches the last call of each entry point enqueues is

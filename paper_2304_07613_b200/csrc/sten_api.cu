@@ -495,10 +495,10 @@ int64_t sten_sparse_linear_host_workspace_size(sten_nmg f, sten_dtype ab_dt, int
            round16(K * ldb * s) + round16(M * ldc * int64_t(dt_size(c_dt)));
 }
 
-sten_status sten_sparse_linear_host(sten_nmg f, sten_dtype ab_dt, const void* W_host, int64_t M, int64_t K,
-                                    int64_t ldw, const void* B_host, int64_t ldb, int64_t N, void* C_host,
-                                    int64_t ldc, sten_dtype c_dt, void* workspace, int64_t workspace_bytes,
-                                    void* stream) {
+static sten_status sparse_linear_host_impl(sten_nmg f, sten_dtype ab_dt, const void* W_host, int64_t M, int64_t K,
+                                          int64_t ldw, const void* B_host, int64_t ldb, int64_t N, void* C_host,
+                                          int64_t ldc, sten_dtype c_dt, void* workspace, int64_t workspace_bytes,
+                                          void* stream, bool sync) {
     sten_status s = check_format(f);
     if (s) return s;
     if (!dtype_ok(ab_dt) || !dtype_ok(c_dt)) return STEN_ERR_INVALID_ARG;
@@ -532,8 +532,24 @@ sten_status sten_sparse_linear_host(sten_nmg f, sten_dtype ab_dt, const void* W_
         cudaMemcpy2DAsync(C_host, size_t(ldc * sc), dC, size_t(dldc * sc), size_t(N * sc), size_t(M),
                           cudaMemcpyDeviceToHost, st) != cudaSuccess)
         return STEN_ERR_CUDA;
-    if (cudaStreamSynchronize(st) != cudaSuccess) return STEN_ERR_CUDA;
+    if (sync && cudaStreamSynchronize(st) != cudaSuccess) return STEN_ERR_CUDA;
     return STEN_OK;
+}
+
+sten_status sten_sparse_linear_host(sten_nmg f, sten_dtype ab_dt, const void* W_host, int64_t M, int64_t K,
+                                    int64_t ldw, const void* B_host, int64_t ldb, int64_t N, void* C_host,
+                                    int64_t ldc, sten_dtype c_dt, void* workspace, int64_t workspace_bytes,
+                                    void* stream) {
+    return sparse_linear_host_impl(f, ab_dt, W_host, M, K, ldw, B_host, ldb, N, C_host, ldc, c_dt, workspace,
+                                   workspace_bytes, stream, true);
+}
+
+sten_status sten_sparse_linear_host_async(sten_nmg f, sten_dtype ab_dt, const void* W_host, int64_t M, int64_t K,
+                                          int64_t ldw, const void* B_host, int64_t ldb, int64_t N, void* C_host,
+                                          int64_t ldc, sten_dtype c_dt, void* workspace, int64_t workspace_bytes,
+                                          void* stream) {
+    return sparse_linear_host_impl(f, ab_dt, W_host, M, K, ldw, B_host, ldb, N, C_host, ldc, c_dt, workspace,
+                                   workspace_bytes, stream, false);
 }
 
 const char* sten_status_string(sten_status s) {

@@ -64,6 +64,8 @@ SIGNATURES = {
     "sten_nmg_densify": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "sten_nmg_spmm": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64, _i64,
                                      _vp, _i64, ctypes.c_int, _vp]),
+    "sten_sparse_linear_host_async": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _i64,
+                                                     _i64, _vp, _i64, ctypes.c_int, _vp, _i64, _vp]),
     "sten_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "sten_algo_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "sten_spmm_launch_count": (ctypes.c_int32, [ctypes.POINTER(sten_spmm_plan)]),
@@ -217,6 +219,19 @@ def sparse_linear_host(W_host: torch.Tensor, B_host: torch.Tensor, n: int, m: in
                                           B_host.data_ptr(), _ld(B_host), N, C_host.data_ptr(), _ld(C_host),
                                           _dt(C_host), workspace.data_ptr(), workspace.numel(), _stream(stream)),
            "sten_sparse_linear_host")
+    return C_host
+
+
+def sparse_linear_host_async(W_host: torch.Tensor, B_host: torch.Tensor, n: int, m: int, g: int,
+                             C_host: torch.Tensor, workspace: torch.Tensor, stream=None) -> torch.Tensor:
+    """sten_sparse_linear_host_async: enqueue H2D, sparsify, SpMM, D2H on `stream`; no wait
+    (pinned host buffers; C_host is valid once the stream has drained)."""
+    M, K = W_host.shape
+    N = B_host.shape[1]
+    _check(load().sten_sparse_linear_host_async(sten_nmg(n, m, g), _dt(W_host), W_host.data_ptr(), M, K,
+                                                _ld(W_host), B_host.data_ptr(), _ld(B_host), N, C_host.data_ptr(),
+                                                _ld(C_host), _dt(C_host), workspace.data_ptr(), workspace.numel(),
+                                                _stream(stream)), "sten_sparse_linear_host_async")
     return C_host
 
 

@@ -279,6 +279,15 @@ def test_host_e2e_entry_point():
     v_ref, i_ref = oracle.sparsify(W, n, m, g)
     C_ref, Bound = oracle.spmm(v_ref, i_ref, B, n, m, g)
     assert rel_err(Ch, C_ref, Bound) <= 1e-5
+    # async variant on two side streams (the bench's e2e path): same bytes once the streams drain
+    Ch2 = torch.zeros((M, N), dtype=torch.float32).pin_memory()
+    Ch3 = torch.zeros((M, N), dtype=torch.float32).pin_memory()
+    ws2 = torch.empty_like(ws)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    sten.sparse_linear_host_async(Wh, Bh, n, m, g, Ch2, ws, stream=s1)
+    sten.sparse_linear_host_async(Wh, Bh, n, m, g, Ch3, ws2, stream=s2)
+    torch.cuda.synchronize()
+    assert torch.equal(Ch2, Ch) and torch.equal(Ch3, Ch)
 
 
 # ----------------------------------------------------------------------------------------
