@@ -409,8 +409,17 @@ def bench_sten(args, rank, world, local_rank):
     flops_step = sum(eff_flops(c) for c in cases)
     value = flops_step * world * args.steps / (total_ms * 1e-3) / 1e9
 
-    # dominant kernel: the SpMM (fp32 -> CUDA-core FFMA bound, bf16 -> tensor / HBM), timed per
-    # launch in the single-stream pass (pass 2) so that launches do not overlap
+    # pass 3 (per-kernel roofline): every case's SpMM and sparsify as R_k back-to-back launches
+    # over rotating input copies (R_k x bytes > 3 x L2: cold L2), CUDA events around the graph
+    # replay on the replaying stream -- a launch's duration without the event-node gaps that the
+    # in-step brackets of pass 2 include
+    b2b = None if args.profile else per_kernel_b2b(cases, sets[0], dtype, device, l2, args.steps)
+    in_step_spmm_ms = [sum(x) / len(x) for x in spmm_ms]
+    in_step_spars_ms = [sum(x) / len(x) for x in spars_ms]
+    if b2b is not None:
+        spmm_ms = [[t] * args.steps for t in b2b["spmm_ms"]]
+        spars_ms = [[t] * args.steps for t in b2b["sparsify_ms"]]
+    # dominant kernel: the SpMM (fp32 -> CUDA-core FFMA bound, bf16 -> tensor / HBM), per launch
     spmm_total_ms = sum(sum(x) for x in spmm_ms)
     spmm_nz = sum(nz_flops(c) for c in cases) * args.steps
     spmm_bytes_tot = sum(spmm_bytes(c) for c in cases) * args.steps
@@ -443,7 +452,9 @@ def bench_sten(args, rank, world, local_rank):
         t = sum(spmm_ms[k]) / len(spmm_ms[k])
         ts = sum(spars_ms[k]) / len(spars_ms[k])
         per_case.append({"case": c.label(), "plan": sets[0][k]["plan"].as_dict(), "spmm_us": round(t * 1e3, 2),
+                         "spmm_us_in_step": round(in_step_spmm_ms[k] * 1e3, 2),
                          "sparsify_us": round(ts * 1e3, 2),
+                         "sparsify_us_in_step": round(in_step_spars_ms[k] * 1e3, 2),
                          "sparsify_gbs": round(sparsify_bytes(c) / (ts * 1e-3) / 1e9, 1),
                          "spmm_eff_gflops": round(eff_flops(c) / (t * 1e-3) / 1e9, 1),
                          "spmm_nz_tflops": round(nz_flops(c) / (t * 1e-3) / 1e12, 3)})
@@ -465,17 +476,21 @@ def bench_sten(args, rank, world, local_rank):
                            "streams in one CUDA graph" % lanes},
         "roofline": roof,
         "spmm_only": {"value": round(sum(eff_flops(c) for c in cases) * args.steps / (spmm_total_ms * 1e-3) / 1e9, 2),
-                      "unit": UNIT, "share_of_step": round(spmm_total_ms / sum(seq_step_ms), 4),
+                      "unit": UNIT,
+                      "share_of_step": round(spmm_total_ms / (spmm_total_ms + sum(sum(x) for x in spars_ms)), 4)
+                      if b2b is not None else round(spmm_total_ms / sum(seq_step_ms), 4),
                       "single_stream_ms_per_step": round(sum(seq_step_ms) / len(seq_step_ms), 5),
-                      "note": "per-launch SpMM times from a second timed pass of the same step on one stream"},
+                      "note": "value: per-launch SpMM times (pass 3 when run, else the in-step brackets); "
+                              "share: SpMM time over SpMM + sparsify time (pass 3; the ncu launch list's "
+                              "share is the cross-check), else over the single-stream step"},
+        "per_kernel_timing": (b2b or {}).get("how", "in-step event brackets of the single-stream graph (pass 2)"),
         "sparsify": {"kernel": "sparsify_grouped_nm_kernel (a1-a3)", "bound": "hbm",
                      "achieved": round(sum(sparsify_bytes(c) for c in cases) * args.steps
                                        / (sum(sum(x) for x in spars_ms) * 1e-3) / 1e9, 1),
                      "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(sum(sparsify_bytes(c) for c in cases) * args.steps
                                    / (sum(sum(x) for x in spars_ms) * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
-                     "note": "algorithmic bytes M*K*s + M*K'*s + idx per launch over the event-timed launch "
-                             "(single-stream pass; includes the graph node gap)"},
+                     "note": "algorithmic bytes M*K*s + M*K'*s + idx per launch over the per-launch time"},
         "per_case": per_case,
         "gpu_launches": launches_per_step * args.steps,
         "loop_ms_device": round(loop_ms, 3),
@@ -485,6 +500,60 @@ def bench_sten(args, rank, world, local_rank):
     if not args.profile:
         out["context_dense"] = dense_context(cases, sets[0], dtype, device)
     return out, cases, host, dtype, g
+
+
+def per_kernel_b2b(cases, data, dtype, device, l2, steps):
+    """Per case: R_k back-to-back SpMM launches (and separately sparsify launches) over R_k
+    rotating copies of the inputs in one CUDA graph; R_k x (bytes one launch touches) > 3 x L2.
+    Returns per-launch ms (median of 3 replays) for every case."""
+    import torch
+    from paper_2304_07613_b200 import sten
+    out_spmm, out_sp = [], []
+    s = esize(dtype)
+    for c, d in zip(cases, data):
+        touch = c.M * c.kept * s + c.Kp * c.N * s + c.M * c.N * s + c.M * c.Kp * s
+        R = int(min(64, max(4, math.ceil(3 * l2 / touch))))
+        Ws = [d["W"].clone() for _ in range(R)]
+        Vs = [d["values"].clone() for _ in range(R)]
+        Is = [d["idx"].clone() for _ in range(R)]
+        Bs = [d["B"].clone() for _ in range(R)]
+        Cs = [torch.empty_like(d["C"]) for _ in range(R)]
+        st = torch.cuda.Stream(device)
+        res = []
+        for which in ("spmm", "sparsify"):
+            def launch(i):
+                if which == "spmm":
+                    sten.spmm_grouped_nm(Vs[i], Is[i], Bs[i], c.n, c.m, c.g, out=Cs[i], plan=d["plan"])
+                else:
+                    sten.sparsify_grouped_nm(Ws[i], c.n, c.m, c.g, values=Vs[i], idx=Is[i])
+            with torch.cuda.stream(st):
+                launch(0)
+            torch.cuda.synchronize()
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph, stream=st):
+                for i in range(R):
+                    launch(i)
+            gph.replay()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                cur = torch.cuda.current_stream()
+                e0.record(cur)
+                gph.replay()                 # replays on the current stream
+                e1.record(cur)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) / R)
+            res.append(sorted(ts)[1])
+            del gph
+        out_spmm.append(res[0])
+        out_sp.append(res[1])
+        del Ws, Vs, Is, Bs, Cs
+    torch.cuda.empty_cache()
+    return {"spmm_ms": out_spmm, "sparsify_ms": out_sp,
+            "how": "pass 3: per case R_k back-to-back launches over R_k rotating input copies (R_k x bytes > "
+                   "3 x L2) in one CUDA graph, CUDA events around the replay on its stream, median of 3; "
+                   "spmm_us_in_step / sparsify_us_in_step = the event brackets inside the single-stream step"}
 
 
 def dense_context(cases, data, dtype, device):
