@@ -70,7 +70,7 @@ def parse_args():
     p.add_argument("--no-tune", action="store_true", help="AUTO plans instead of sten_spmm_autotune")
     p.add_argument("--plans-out", default=None, help="write the per-case plans used to this JSON file")
     p.add_argument("--plans-in", default=None, help="use the per-case plans of this JSON file (no tuning)")
-    p.add_argument("--lanes", type=int, default=3,
+    p.add_argument("--lanes", type=int, default=9,
                    help="streams the independent cases of a step are spread over (inside the graph)")
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu legs)")
     p.add_argument("--out", default=None, help="also append the JSON line to this file")
