@@ -103,6 +103,16 @@ sten_status sten_sparsify_grouped_nm(sten_nmg f, sten_dtype dt,
                                      const void* W, int64_t M, int64_t K, int64_t ldw,
                                      void* values, uint8_t* idx, void* stream);
 
+/* NEXT-2 SameFormat re-sparsification: re-pack a new dense W
+ * [M][ldw] (e.g. the weights after an optimizer step) with an EXISTING pattern idx, so the
+ * format stays fixed: values[r][kb*n+t] = W[r][kb*m + idx[r/g][kb][t]] (bit copies).
+ *   idx    [M/g][K/m][n] uint8 (input, as produced by sten_sparsify_grouped_nm)
+ *   values [M][K/m*n] dtype dt (output, overwritten)
+ * idx entries must be < m (not checked on the device). */
+sten_status sten_resparsify_same_format(sten_nmg f, sten_dtype dt,
+                                        const void* W, int64_t M, int64_t K, int64_t ldw,
+                                        const uint8_t* idx, void* values, void* stream);
+
 /* a4: grouped n:m -> dense.  W_out [M][ldw] receives zeros at
  * pruned positions and the stored values at kept ones (columns >= K untouched). */
 sten_status sten_densify(sten_nmg f, sten_dtype dt,

@@ -50,6 +50,7 @@ def _load():
         lib.oracle_dense_matmul.argtypes = [ctypes.c_int, _ptr, _i64, _i64, _i64, _ptr, _i64, _i64,
                                             _ptr, ctypes.c_int]
         lib.oracle_energy.argtypes = [ctypes.c_int, _ptr, _ptr, _i64, _i64, _i64]
+        lib.oracle_same_format.argtypes = [ctypes.c_int] * 4 + [_ptr, _i64, _i64, _i64, _ptr, _ptr]
         lib.oracle_nmg_patterns.argtypes = [ctypes.c_int, ctypes.c_int, _ptr]
         lib.oracle_nmg_sparsify.argtypes = [ctypes.c_int] * 4 + [_ptr, _i64, _i64, _i64, _ptr, _ptr]
         lib.oracle_nmg_densify.argtypes = [ctypes.c_int] * 4 + [_ptr, _ptr, _i64, _i64, _ptr, _i64]
@@ -264,3 +265,14 @@ def nmg_brute_best_energy(W_int: np.ndarray, n: int, m: int, g: int) -> float:
 
     rec(0, [0] * len(pats), 0.0)
     return best
+
+
+def same_format(W: np.ndarray, idx: np.ndarray, n: int, m: int, g: int) -> np.ndarray:
+    """SameFormat re-sparsification: values of W at an existing pattern idx."""
+    W = np.ascontiguousarray(W)
+    idx = np.ascontiguousarray(idx, dtype=np.uint8)
+    M, K = W.shape
+    values = np.zeros((M, K // m * n), dtype=W.dtype)
+    _check(_load().oracle_same_format(n, m, g, _dtype_code(W), _p(W), M, K, K, _p(idx), _p(values)),
+           "same_format")
+    return values

@@ -430,3 +430,23 @@ int oracle_nmg_spmm(int n, int m, int g, int dtype, const void* values, const ui
     free(pos);
     return 0;
 }
+
+/* SameFormat re-sparsification (NEXT-2): re-pack a new dense W' with an EXISTING grouped n:m
+ * pattern -- "The new tensor is sparsified using the SameFormatSparsifier to maintain the same
+ * format it had before" (the fixed-pattern fast path):
+ *   values[r][kb*n+t] = W'[r][kb*m + idx[r/g][kb][t]]                                      */
+int oracle_same_format(int n, int m, int g, int dtype, const void* W, int64_t M, int64_t K, int64_t ldw,
+                       const uint8_t* idx, void* values)
+{
+    int rc = check_args(n, m, g, dtype, M, K);
+    if (rc) return rc;
+    if (ldw < K) return 2;
+    int64_t KB = K / m, Kp = KB * n;
+    for (int64_t r = 0; r < M; ++r)
+        for (int64_t kb = 0; kb < KB; ++kb)
+            for (int t = 0; t < n; ++t) {
+                int j = idx[((r / g) * KB + kb) * n + t];
+                copy_elem(dtype, values, r * Kp + kb * n + t, W, r * ldw + kb * m + j);
+            }
+    return 0;
+}

@@ -256,6 +256,32 @@ sparsify_grouped_nm_kernel(const T* __restrict__ W, int64_t ldw, int64_t G, int6
     else sparsify_body<T, MB, NK, 0>(W, ldw, grp, kb, KB, n, g, values, Kp, idx);
 }
 
+// NEXT-2 SameFormat re-sparsification: re-pack a new dense W' with an EXISTING pattern
+// ("the new tensor is sparsified using the SameFormatSparsifier to maintain the same format",
+// PAPER.md:398): values[r][kb n + t] = W'[r][kb m + idx[r/g][kb][t]].  One thread per
+// (row, m-block): one vector load of the block, n selects, n stores.  HBM-bound like K1.
+template <typename T, int MB>
+__global__ void __launch_bounds__(256)
+same_format_grouped_nm_kernel(const T* __restrict__ W, int64_t ldw, int64_t M, int64_t KB, int n, int g,
+                              const uint8_t* __restrict__ idx, T* __restrict__ values, int64_t Kp, int aligned) {
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= M * KB) return;
+    const int64_t r = tid / KB, kb = tid - r * KB;
+    T row[MB];
+    if (aligned == 2) load_block<T, MB>(W + r * ldw + kb * MB, row, 2);
+    else if (aligned == 1) load_block<T, MB>(W + r * ldw + kb * MB, row, 1);
+    else load_block<T, MB>(W + r * ldw + kb * MB, row, 0);
+    const uint8_t* ip = idx + ((r / g) * KB + kb) * n;
+    T* vp = values + r * Kp + kb * n;
+    for (int t = 0; t < n; ++t) {
+        const int j = ip[t];
+        T v = row[0];
+#pragma unroll
+        for (int q = 1; q < MB; ++q) v = j == q ? row[q] : v;
+        vp[t] = v;
+    }
+}
+
 // K2 densify: one thread per (row, m-block); writes the full m-element block
 // (zeros at pruned positions) with one vector store when aligned.
 template <typename T, int MB>

@@ -441,6 +441,39 @@ sten_status sten_sparsify_grouped_nm(sten_nmg f, sten_dtype dt, const void* W, i
     return last_cuda();
 }
 
+sten_status sten_resparsify_same_format(sten_nmg f, sten_dtype dt, const void* W, int64_t M, int64_t K,
+                                        int64_t ldw, const uint8_t* idx, void* values, void* stream) {
+    sten_status s = check_format(f);
+    if (s) return s;
+    if (!dtype_ok(dt)) return STEN_ERR_INVALID_ARG;
+    if ((s = check_shape(f, M, K))) return s;
+    if (ldw < K) return STEN_ERR_SHAPE;
+    if (M * K > 0 && (!W || !values || !idx)) return STEN_ERR_INVALID_ARG;
+    const int64_t KB = K / f.m, Kp = KB * f.n;
+    if (M == 0 || KB == 0) return STEN_OK;
+    const int64_t ldw_bytes = ldw * int64_t(dt_size(dt));
+    const uintptr_t wa = reinterpret_cast<uintptr_t>(W);
+    const int aligned = (wa % 32 == 0 && ldw_bytes % 32 == 0) ? 2 : (wa % 16 == 0 && ldw_bytes % 16 == 0) ? 1 : 0;
+    cudaStream_t st = as_stream(stream);
+    const unsigned grid = grid1d(M * KB);
+#define STEN_SF_CASE(MBV)                                                                                      \
+    case MBV:                                                                                                 \
+        if (dt == STEN_F32)                                                                                   \
+            same_format_grouped_nm_kernel<float, MBV><<<grid, 256, 0, st>>>(                                  \
+                static_cast<const float*>(W), ldw, M, KB, f.n, f.g, idx, static_cast<float*>(values), Kp, aligned); \
+        else                                                                                                  \
+            same_format_grouped_nm_kernel<bf16_t, MBV><<<grid, 256, 0, st>>>(                                 \
+                static_cast<const bf16_t*>(W), ldw, M, KB, f.n, f.g, idx, static_cast<bf16_t*>(values), Kp, aligned); \
+        break;
+    switch (f.m) {
+        STEN_SF_CASE(2) STEN_SF_CASE(4) STEN_SF_CASE(6) STEN_SF_CASE(8) STEN_SF_CASE(10) STEN_SF_CASE(12)
+        STEN_SF_CASE(16)
+        default: return STEN_ERR_UNSUPPORTED;
+    }
+#undef STEN_SF_CASE
+    return last_cuda();
+}
+
 sten_status sten_densify(sten_nmg f, sten_dtype dt, const void* values, const uint8_t* idx, int64_t M,
                          int64_t K, void* W_out, int64_t ldw, void* stream) {
     sten_status s = check_format(f);

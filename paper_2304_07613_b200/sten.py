@@ -66,6 +66,8 @@ SIGNATURES = {
                                      _vp, _i64, ctypes.c_int, _vp]),
     "sten_sparse_linear_host_async": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _i64,
                                                      _i64, _vp, _i64, ctypes.c_int, _vp, _i64, _vp]),
+    "sten_resparsify_same_format": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _vp,
+                                                   _vp]),
     "sten_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "sten_algo_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "sten_spmm_launch_count": (ctypes.c_int32, [ctypes.POINTER(sten_spmm_plan)]),
@@ -144,6 +146,19 @@ def sparsify_grouped_nm(W: torch.Tensor, n: int, m: int, g: int, values: torch.T
                                            values.data_ptr(), idx.data_ptr(), _stream(stream)),
            "sten_sparsify_grouped_nm")
     return values, idx
+
+
+def resparsify_same_format(W: torch.Tensor, idx: torch.Tensor, n: int, m: int, g: int,
+                           values: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """NEXT-2 SameFormat: values of a new dense W [M][K] at the existing pattern idx."""
+    _cuda(W, "W")
+    M, K = W.shape
+    if values is None:
+        values = torch.empty((M, K // m * n), dtype=W.dtype, device=W.device)
+    _check(load().sten_resparsify_same_format(sten_nmg(n, m, g), _dt(W), W.data_ptr(), M, K, _ld(W),
+                                              idx.data_ptr(), values.data_ptr(), _stream(stream)),
+           "sten_resparsify_same_format")
+    return values
 
 
 def densify(values: torch.Tensor, idx: torch.Tensor, n: int, m: int, g: int, K: int,

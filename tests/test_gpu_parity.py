@@ -413,3 +413,21 @@ def test_spmm_autotune(dtype, g):
     assert plan.algo in (sten.ALGO_SIMT, sten.ALGO_MMA_SYNC, sten.ALGO_TCGEN05)
     C = sten.spmm_grouped_nm(v, i, Bd, n, m, g, out_dtype=torch.float32, plan=plan)
     assert rel_err(C, C_ref, Bound) <= 1e-5
+
+
+# ----------------------------------------------------------------------------------------
+# NEXT-2: SameFormat re-sparsification -- bit-exact vs the oracle
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n,m,g", [(2, 4, 4), (1, 4, 1), (1, 10, 2), (3, 6, 3), (2, 8, 4), (4, 16, 1)])
+@pytest.mark.parametrize("ld_multiple", [1, 8])
+def test_resparsify_same_format_bit_exact(dtype, n, m, g, ld_multiple):
+    M, K = 10 * g, 23 * m
+    W = synthetic.weights(M, K, seed=n + m + g, dtype=dtype)
+    W2 = synthetic.weights(M, K, seed=1000 + n + m + g, dtype=dtype)     # "after an optimizer step"
+    _, i = gpu_sparsify(W, n, m, g, dtype)
+    v2 = sten.resparsify_same_format(dev(W2, dtype, ld_multiple=ld_multiple), i, n, m, g)
+    torch.cuda.synchronize()
+    _, i_ref = oracle.sparsify(W, n, m, g)
+    v2_ref = oracle.same_format(W2, i_ref, n, m, g)
+    assert np.array_equal(host(v2).view(np.uint8), v2_ref.view(np.uint8))

@@ -276,3 +276,25 @@ def test_fp32_score_rounding_decides_near_ties():
     W2 = _f32([[1.0, 1.0 + 2.0 ** -23], [e, 0.0], [e, 0.0]])
     _, idx2 = oracle.sparsify(W2, 1, 2, 3)
     assert idx2.tolist() == [[[1]]]      # exact sums: col0 = 1 + 2^-23 == col1, but fp32 col0 = 1.0
+
+
+# ----------------------------------------------------------------------------------------
+# NEXT-2: SameFormat re-sparsification
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("n,m,g", [(2, 4, 4), (1, 4, 1), (1, 10, 2), (3, 6, 3)])
+def test_same_format_pins(n, m, g):
+    W = synthetic.weights(6 * g, 5 * m, seed=n + m + g)
+    v, i = oracle.sparsify(W, n, m, g)
+    # on the tensor that produced the pattern, re-packing gives the sparsifier's own values
+    assert np.array_equal(oracle.same_format(W, i, n, m, g), v)
+    # on a new tensor W2 (e.g. after an optimizer step): densify(re-pack) = W2 masked by the OLD
+    # pattern; the mask is read off the densified all-ones tensor (independent of W2)
+    W2 = synthetic.weights(6 * g, 5 * m, seed=99 + n + m + g)
+    v2 = oracle.same_format(W2, i, n, m, g)
+    mask = oracle.densify(np.ones_like(v), i, n, m, g, W.shape[1]) != 0
+    assert np.array_equal(oracle.densify(v2, i, n, m, g, W.shape[1]), np.where(mask, W2, 0).astype(np.float32))
+    assert (mask.reshape(W.shape[0], -1, m).sum(axis=2) == n).all()
+    # bf16 bytes are copied bit for bit
+    Wb = synthetic.weights(6 * g, 5 * m, seed=7, dtype="bf16")
+    vb, ib = oracle.sparsify(Wb, n, m, g)
+    assert np.array_equal(oracle.same_format(Wb, ib, n, m, g), vb)

@@ -31,7 +31,8 @@ for (M, K, n, m, g) in [(768, 768, 2, 4, 4), (768, 3072, 2, 4, 4), (3072, 768, 1
     warm = timeit(lambda i: sten.sparsify_grouped_nm(Ws[0], n, m, g, values=vals, idx=idx))
     cold = timeit(f)
     cp = timeit(lambda i: dst.copy_(Ws[i % R][:, : K // m * n]))
+    sf = timeit(lambda i: sten.resparsify_same_format(Ws[i % R], idx, n, m, g, values=vals))
     byts = M * K * 4 + M * K // m * n * 4 + M // g * K // m * n
-    out.append(dict(shape=[M, K, n, m, g], warm_us=round(warm, 2), cold_us=round(cold, 2), copy_us=round(cp, 2),
+    out.append(dict(shape=[M, K, n, m, g], warm_us=round(warm, 2), cold_us=round(cold, 2), copy_us=round(cp, 2), same_format_us=round(sf, 2),
                     cold_gbs=round(byts / cold / 1e3, 1)))
     print(json.dumps(out[-1]), flush=True)
