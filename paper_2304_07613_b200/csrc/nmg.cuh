@@ -8,6 +8,7 @@
 //   values  [M/m][K/L][L][n], idx [M/m][K/L][L] uint16 (original column in the chunk)
 #pragma once
 #include "common.cuh"
+#include "spmm_simt.cuh"   // SpmmArgs, cluster_reduce_store (split-K over DSMEM)
 
 namespace sten {
 
@@ -196,17 +197,20 @@ __global__ void __launch_bounds__(256) nmg_densify_kernel(const NmgArgs a, T* __
 }
 
 // ---- product (Fig. 5) ----------------------------------------------------------------------------
-// CTA = 16 warps x BN = 128 tokens (lane: 4 consecutive tokens); warp w owns row block rb0 + w (m
-// rows; accumulators acc[m][4] in registers with static row indices, because the pattern order
+// CTA = 8 warps x BN = 256 tokens (lane: 8 tokens, two 16-byte vectors 512 B apart for fp32, so a
+// warp's gathered row read is two conflict-free 512-byte passes); warp w owns row block rbc + w
+// (m rows; accumulators acc[m][8] in registers with static row indices, because the pattern order
 // is a compile-time table -- "chunks, which fix the order of sparsity permutations, allow kernels
-// to avoid branches based on the sparsity structure").  A K-stage of CPS whole
-// chunks is staged in shared memory by cp.async (double buffered): the CPS L rows of B (shared by
-// the CTA's 16 row blocks) and, per row block, its CPS L idx entries and CPS L n values.  Per slot
-// a warp reads the idx (broadcast), gathers its B row (LDS.128 for fp32), reads the n values
-// (broadcast) and does 4 n FMAs per lane -- "loaded from sparse values, then broadcast into vector
-// registers ... indirect loads from specific rows of B ... FMA".  Each gathered
-// B element feeds n FMAs (the (A) layout's gathered element feeds g), so for fp32 the shared-memory
-// datapath caps this kernel at ~n/4 of the FFMA peak.
+// to avoid branches based on the sparsity structure").  A K-stage of CPS whole chunks
+// is staged by cp.async in a 3-stage ring: the CPS L rows of B (shared by the CTA's 8 row blocks)
+// and, per row block, its CPS L idx entries and CPS L n values.  Per slot a warp reads the idx
+// (broadcast), gathers its B row, reads the n values (broadcast) and does 4n FFMA2 per lane --
+// "loaded from sparse values, then broadcast into vector registers ... indirect loads from
+// specific rows of B ... FMA".  Split-K over whole chunks: the S CTAs of a tile
+// form a thread-block cluster (1,1,S) and reduce their fp32 partial tiles over DSMEM in the fixed
+// order z = 0..S-1 (the (A) kernel's cluster_reduce_store), so the result is deterministic.
+// Each gathered B element feeds n FMAs (the (A) layout's feeds g), so for fp32 the shared-memory
+// datapath caps this kernel near n/4 of the FFMA peak.
 struct NmgSpmmArgs {
     const void* values;
     const uint16_t* idx;
@@ -214,11 +218,13 @@ struct NmgSpmmArgs {
     void* C;
     int64_t M, K, N, ldb, ldc, NC, RB;
     int g, L, cps;          // cps = chunks per K-stage
+    int split;              // S: split-K parts (cluster z extent)
+    bool c_vec;
 };
 
-constexpr int kNmgSpmmWarps = 16;
+constexpr int kNmgSpmmWarps = 8;
 constexpr int kNmgStages = 3;
-constexpr int kNmgBN = 128;
+constexpr int kNmgBN = 256;
 
 // per-stage shared memory: B [cps L][BN] | idx [8][cps L] u16 | values [8][cps L n]
 template <typename TAB>
@@ -230,40 +236,42 @@ __host__ __device__ inline size_t nmg_spmm_stage_bytes(int rows, int n) {
 }
 
 template <typename TAB, typename TC, int NN, int MM>
-__global__ void __launch_bounds__(kNmgSpmmWarps * 32)
+__global__ void __launch_bounds__(kNmgSpmmWarps * 32, 2)
 nmg_spmm_kernel(const NmgSpmmArgs a) {
     constexpr NmgPatterns P = nmg_revolving_door(MM, NN);
     constexpr int CP = nmg_binom(MM, NN);
     static_assert(CP <= kNmgMaxPatterns, "too many patterns");
-    constexpr int EV = 4;                                   // tokens per lane
+    constexpr int EV = 8;                                   // tokens per lane
     constexpr int NT = kNmgSpmmWarps * 32;
+    constexpr int ROWB = kNmgBN * int(sizeof(TAB));         // bytes per staged B row
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t n0 = int64_t(blockIdx.x) * kNmgBN;
     const int64_t rbc = int64_t(blockIdx.y) * kNmgSpmmWarps;          // first row block of the CTA
     const int L = a.L, g = a.g;
     const int rows = a.cps * L;                                        // B rows per stage
-    const size_t b_bytes = size_t(rows) * kNmgBN * sizeof(TAB);
+    const size_t b_bytes = size_t(rows) * ROWB;
     const size_t i_bytes = (size_t(kNmgSpmmWarps) * rows * 2 + 15) & ~size_t(15);
     const size_t stage_bytes = nmg_spmm_stage_bytes<TAB>(rows, NN);
     const TAB* B = static_cast<const TAB*>(a.B);
     const TAB* V = static_cast<const TAB*>(a.values);
-    const int64_t nstages = (a.NC + a.cps - 1) / a.cps;
+    // split-K part z: chunks [z NC / S, (z+1) NC / S), staged cps at a time
+    const int64_t c_lo = a.NC * int64_t(blockIdx.z) / a.split, c_hi = a.NC * int64_t(blockIdx.z + 1) / a.split;
+    const int64_t nstages = (c_hi - c_lo + a.cps - 1) / a.cps;
 
     auto load_stage = [&](int64_t st, int buf) {
         unsigned char* dst = smem + size_t(buf) * stage_bytes;
-        const int64_t c0 = st * a.cps;
-        const int nch = int(min64(a.cps, a.NC - c0));
+        const int64_t c0 = c_lo + st * a.cps;
+        const int nch = int(min64(a.cps, c_hi - c0));
         const int64_t k0 = c0 * L;
-        constexpr int CH = kNmgBN * int(sizeof(TAB)) / 16;            // 16-byte chunks per B row
+        constexpr int CH = ROWB / 16;                                  // 16-byte chunks per B row
         for (int e = threadIdx.x; e < rows * CH; e += NT) {
             const int r = e / CH, ch = e - r * CH;
             const int64_t k = k0 + r;
             const int64_t col = n0 + int64_t(ch) * (16 / int(sizeof(TAB)));
             int bytes = 0;
             if (r < nch * L && col < a.N) bytes = int(min64(16, (a.N - col) * int64_t(sizeof(TAB))));
-            cp_async16(dst + size_t(r) * kNmgBN * sizeof(TAB) + size_t(ch) * 16, bytes ? B + k * a.ldb + col : B,
-                       bytes);
+            cp_async16(dst + size_t(r) * ROWB + size_t(ch) * 16, bytes ? B + k * a.ldb + col : B, bytes);
         }
         // idx and values of the CTA's row blocks: contiguous runs (4-byte words; L is even for
         // every compiled format, so runs start and end on 4-byte boundaries)
@@ -305,57 +313,79 @@ nmg_spmm_kernel(const NmgSpmmArgs a) {
         else cp_async_commit();
         if (rb < a.RB) {
             const unsigned char* sb = smem + size_t(buf) * stage_bytes;
-            const uint32_t sB = smem_u32(sb) + uint32_t(lane) * EV * uint32_t(sizeof(TAB));
+            const uint32_t sB = smem_u32(sb) + uint32_t(lane) * 16u;
             const uint16_t* sI = reinterpret_cast<const uint16_t*>(sb + b_bytes) + size_t(warp) * rows;
             const TAB* sV = reinterpret_cast<const TAB*>(sb + b_bytes + i_bytes) + size_t(warp) * rows * NN;
-            const int nch = int(min64(a.cps, a.NC - st * a.cps));
+            const int nch = int(min64(a.cps, c_hi - (c_lo + st * a.cps)));
             for (int cl = 0; cl < nch; ++cl) {
-                const uint32_t sBc = sB + uint32_t(cl * L) * kNmgBN * uint32_t(sizeof(TAB));
+                const uint32_t sBc = sB + uint32_t(cl * L) * uint32_t(ROWB);
                 const uint16_t* ip = sI + cl * L;
                 const TAB* vp = sV + size_t(cl) * L * NN;
 #pragma unroll
                 for (int p = 0; p < CP; ++p) {
-#pragma unroll 4
+#pragma unroll 2
                     for (int j = 0; j < g; ++j) {
                         const int s = p * g + j;
-                        const uint32_t addr = sBc + uint32_t(ip[s]) * kNmgBN * uint32_t(sizeof(TAB));
-                        float2 b01, b23;
+                        const uint32_t addr = sBc + uint32_t(ip[s]) * uint32_t(ROWB);
+                        float2 b[4];
                         if constexpr (sizeof(TAB) == 4) {
-                            const float4 t4 = lds128_addr(addr);
-                            b01 = make_float2(t4.x, t4.y);
-                            b23 = make_float2(t4.z, t4.w);
+                            const float4 x0 = lds128_addr(addr), x1 = lds128_addr(addr + 512u);
+                            b[0] = make_float2(x0.x, x0.y); b[1] = make_float2(x0.z, x0.w);
+                            b[2] = make_float2(x1.x, x1.y); b[3] = make_float2(x1.z, x1.w);
                         } else {
-                            uint32_t w0, w1;
-                            asm("ld.shared.v2.u32 {%0,%1}, [%2];\n" : "=r"(w0), "=r"(w1) : "r"(addr));
-                            b01 = make_float2(__uint_as_float(w0 << 16), __uint_as_float(w0 & 0xffff0000u));
-                            b23 = make_float2(__uint_as_float(w1 << 16), __uint_as_float(w1 & 0xffff0000u));
+                            const float4 x = lds128_addr(addr);
+                            const uint32_t w[4] = {__float_as_uint(x.x), __float_as_uint(x.y),
+                                                   __float_as_uint(x.z), __float_as_uint(x.w)};
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                b[q] = make_float2(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u));
                         }
 #pragma unroll
                         for (int t = 0; t < NN; ++t) {
                             const float v = to_f32(vp[s * NN + t]);
                             const int r = nmg_pos(P.mask[p], t);
-                            float2& c01 = *reinterpret_cast<float2*>(&acc[r][0]);
-                            float2& c23 = *reinterpret_cast<float2*>(&acc[r][2]);
-                            c01 = __ffma2_rn(make_float2(v, v), b01, c01);
-                            c23 = __ffma2_rn(make_float2(v, v), b23, c23);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                float2& c2 = *reinterpret_cast<float2*>(&acc[r][2 * q]);
+                                c2 = __ffma2_rn(make_float2(v, v), b[q], c2);
+                            }
                         }
                     }
                 }
             }
         }
     }
-    if (rb >= a.RB) return;
-    // epilogue: rows rb m + r, tokens n0 + 4 lane + e
-    TC* Cp = static_cast<TC*>(a.C);
+    // token of accumulator e: fp32 -> n0 + 4 lane + (e & 3) + 128 (e >> 2); bf16 -> n0 + 8 lane + e
+    auto col_of = [&](int e) -> int {
+        return sizeof(TAB) == 4 ? 4 * lane + (e & 3) + 128 * (e >> 2) : 8 * lane + e;
+    };
+    if (a.split == 1) {
+        if (rb >= a.RB) return;
+        TC* Cp = static_cast<TC*>(a.C);
 #pragma unroll
-    for (int r = 0; r < MM; ++r) {
-        TC* row = Cp + (rb * MM + r) * a.ldc;
+        for (int r = 0; r < MM; ++r) {
+            TC* row = Cp + (rb * MM + r) * a.ldc;
 #pragma unroll
-        for (int e = 0; e < EV; ++e) {
-            const int64_t col = n0 + int64_t(lane) * EV + e;
-            if (col < a.N) row[col] = from_f32<TC>(acc[r][e]);
+            for (int e = 0; e < EV; ++e) {
+                const int64_t col = n0 + col_of(e);
+                if (col < a.N) row[col] = from_f32<TC>(acc[r][e]);
+            }
         }
+        return;
     }
+    // split-K: park the fp32 partial tile [8 MM][BN] at the start of shared memory, reduce over the
+    // cluster in the fixed order z = 0..S-1
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    float* tile = reinterpret_cast<float*>(smem);
+#pragma unroll
+    for (int r = 0; r < MM; ++r)
+#pragma unroll
+        for (int e = 0; e < EV; ++e) tile[(warp * MM + r) * kNmgBN + col_of(e)] = acc[r][e];
+    SpmmArgs ra;
+    memset(&ra, 0, sizeof(ra));
+    ra.C = a.C; ra.M = a.M; ra.N = a.N; ra.ldc = a.ldc; ra.split = a.split; ra.c_vec = a.c_vec;
+    cluster_reduce_store<TC, kNmgSpmmWarps * MM, kNmgBN, NT>(smem, ra, rbc * MM, n0);
 }
 
 }  // namespace sten

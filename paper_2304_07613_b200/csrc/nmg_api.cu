@@ -34,16 +34,34 @@ sten_status nmg_setup(sten_nmg f, int dt, int64_t M, int64_t K, NmgArgs* a) {
 template <typename TAB, typename TC, int NN, int MM>
 sten_status launch_nmg_spmm(const NmgSpmmArgs& a0, cudaStream_t st) {
     NmgSpmmArgs a = a0;
-    a.cps = a.L >= 64 ? 1 : (64 + a.L - 1) / a.L;                   // >= 64 B rows per K-stage
+    a.cps = a.L >= 32 ? 1 : (32 + a.L - 1) / a.L;                   // >= 32 B rows per K-stage
     if (a.cps > a.NC) a.cps = int(a.NC > 0 ? a.NC : 1);
-    while (a.cps > 1 && kNmgStages * nmg_spmm_stage_bytes<TAB>(a.cps * a.L, NN) > 227 * 1024) --a.cps;
-    const size_t smem = kNmgStages * nmg_spmm_stage_bytes<TAB>(a.cps * a.L, NN);
+    while (a.cps > 1 && kNmgStages * nmg_spmm_stage_bytes<TAB>(a.cps * a.L, NN) > 113 * 1024) --a.cps;
+    size_t smem = kNmgStages * nmg_spmm_stage_bytes<TAB>(a.cps * a.L, NN);
+    const size_t tile = size_t(kNmgSpmmWarps) * MM * kNmgBN * 4;    // split-K partial tile (fp32)
+    const int64_t gx = (a.N + kNmgBN - 1) / kNmgBN, gy = (a.RB + kNmgSpmmWarps - 1) / kNmgSpmmWarps;
+    // split-K (cluster z) until about two CTAs per SM: S <= 8 (portable cluster), <= chunks
+    int S = 1;
+    while (S < 8 && gx * gy * S < 2 * 148 && a.NC >= 2 * (S + 1)) ++S;
+    a.split = S;
+    if (S > 1 && smem < tile) smem = tile;
     if (smem > 227 * 1024) return STEN_ERR_UNSUPPORTED;
     auto kern = nmg_spmm_kernel<TAB, TC, NN, MM>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
         return STEN_ERR_CUDA;
-    dim3 grid(unsigned((a.N + kNmgBN - 1) / kNmgBN), unsigned((a.RB + kNmgSpmmWarps - 1) / kNmgSpmmWarps));
-    kern<<<grid, kNmgSpmmWarps * 32, smem, st>>>(a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(gx), unsigned(gy), unsigned(S));
+    cfg.blockDim = dim3(kNmgSpmmWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = unsigned(S);
+    cfg.attrs = attr;
+    cfg.numAttrs = S > 1 ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return STEN_ERR_CUDA;
     return nmg_last_cuda();
 }
 
@@ -138,6 +156,7 @@ sten_status sten_nmg_spmm(sten_nmg f, sten_dtype ab_dt, const void* values, cons
     a.values = values; a.idx = idx; a.B = B; a.C = C;
     a.M = M; a.K = K; a.N = N; a.ldb = ldb; a.ldc = ldc; a.NC = fa.NC; a.RB = fa.RB;
     a.g = f.g; a.L = fa.L;
+    a.c_vec = (reinterpret_cast<uintptr_t>(C) & 15u) == 0 && (ldc * int64_t(nmg_dt_size(c_dt))) % 16 == 0;
     if (ab_dt == STEN_F32)
         return c_dt == STEN_F32 ? dispatch_nmg_spmm<float, float>(f.n, f.m, a, st)
                                 : dispatch_nmg_spmm<float, uint16_t>(f.n, f.m, a, st);
