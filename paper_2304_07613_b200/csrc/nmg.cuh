@@ -81,7 +81,9 @@ __host__ __device__ inline size_t nmg_warp_smem(int L, int C, int m, int esz) {
     return keys + w + ((size_t(C) * 4 + size_t(L) * 2 + 15) & ~size_t(15));
 }
 
-template <typename T>
+// KPL = keys per lane held in registers (2, 4, 6 or 8: the smallest with 32 KPL >= L C); for
+// L C > 256 the keys live in shared memory (KPL unused)
+template <typename T, int KPL>
 __global__ void __launch_bounds__(kNmgWarpsPerCta * 32)
 nmg_sparsify_kernel(const NmgArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -127,15 +129,15 @@ nmg_sparsify_kernel(const NmgArgs a) {
     auto kb = [](unsigned long long k) { return int(0xFFFFu - uint32_t((k >> 16) & 0xFFFFu)); };
     auto kp = [](unsigned long long k) { return int(0xFFFFu - uint32_t(k & 0xFFFFu)); };
 
-    if (NI <= 32 * kNmgRegKeys) {
+    if (NI <= 32 * KPL) {
         // keys in registers; a key is zeroed when its column is taken or its pattern is full
-        unsigned long long kr[kNmgRegKeys];
+        unsigned long long kr[KPL];
 #pragma unroll
-        for (int j = 0; j < kNmgRegKeys; ++j) kr[j] = lane + 32 * j < NI ? make_key(lane + 32 * j) : 0ull;
+        for (int j = 0; j < KPL; ++j) kr[j] = lane + 32 * j < NI ? make_key(lane + 32 * j) : 0ull;
         for (int step = 0; step < L; ++step) {
             unsigned long long best = 0ull;
 #pragma unroll
-            for (int j = 0; j < kNmgRegKeys; ++j) best = kr[j] > best ? kr[j] : best;
+            for (int j = 0; j < KPL; ++j) best = kr[j] > best ? kr[j] : best;
             best = warp_max(best);
             const int b = kb(best), p = kp(best);
             const int c_old = cnt[p];
@@ -144,7 +146,7 @@ nmg_sparsify_kernel(const NmgArgs a) {
             __syncwarp();
             const bool full = c_old + 1 >= g;
 #pragma unroll
-            for (int j = 0; j < kNmgRegKeys; ++j)
+            for (int j = 0; j < KPL; ++j)
                 if (kr[j] != 0ull && (kb(kr[j]) == b || (full && kp(kr[j]) == p))) kr[j] = 0ull;
         }
     } else {

@@ -99,17 +99,27 @@ sten_status sten_nmg_sparsify(sten_nmg f, sten_dtype dt, const void* W, int64_t 
     const size_t smem = size_t(kNmgWarpsPerCta) * nmg_warp_smem(a.L, a.C, a.m, int(nmg_dt_size(dt)));
     const unsigned grid = unsigned((chunks + kNmgWarpsPerCta - 1) / kNmgWarpsPerCta);
     cudaStream_t st = nmg_stream(stream);
+    const int NI = a.L * a.C;
+    const int kpl = NI <= 64 ? 2 : NI <= 128 ? 4 : NI <= 192 ? 6 : 8;
+    auto go = [&](auto kern) -> sten_status {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) return STEN_ERR_CUDA;
+        kern<<<grid, kNmgWarpsPerCta * 32, smem, st>>>(a);
+        return nmg_last_cuda();
+    };
     if (dt == STEN_F32) {
-        if (cudaFuncSetAttribute(nmg_sparsify_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)))
-            return STEN_ERR_CUDA;
-        nmg_sparsify_kernel<float><<<grid, kNmgWarpsPerCta * 32, smem, st>>>(a);
-    } else {
-        if (cudaFuncSetAttribute(nmg_sparsify_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem)))
-            return STEN_ERR_CUDA;
-        nmg_sparsify_kernel<uint16_t><<<grid, kNmgWarpsPerCta * 32, smem, st>>>(a);
+        switch (kpl) {
+            case 2: return go(nmg_sparsify_kernel<float, 2>);
+            case 4: return go(nmg_sparsify_kernel<float, 4>);
+            case 6: return go(nmg_sparsify_kernel<float, 6>);
+            default: return go(nmg_sparsify_kernel<float, 8>);
+        }
     }
-    return nmg_last_cuda();
+    switch (kpl) {
+        case 2: return go(nmg_sparsify_kernel<uint16_t, 2>);
+        case 4: return go(nmg_sparsify_kernel<uint16_t, 4>);
+        case 6: return go(nmg_sparsify_kernel<uint16_t, 6>);
+        default: return go(nmg_sparsify_kernel<uint16_t, 8>);
+    }
 }
 
 sten_status sten_nmg_densify(sten_nmg f, sten_dtype dt, const void* values, const uint16_t* idx, int64_t M,
