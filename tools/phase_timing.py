@@ -16,7 +16,8 @@ def build(exp=0, defs="", tag=""):
     from paper_2304_07613_b200 import build as b
     extra = ["-D" + d for d in defs.split(",") if d]
     cmd = [b.NVCC] + b.ARCH + b.FLAGS + ["-DSTEN_TIMING", "-DSTEN_TC_EXP=%d" % exp] + extra + [
-        "-I", b.INCLUDE, "-I", b.CSRC, "-o", lib_path(exp, tag), os.path.join(b.CSRC, "sten_api.cu")]
+        "-I", b.INCLUDE, "-I", b.CSRC, "-o", lib_path(exp, tag)] + sorted(
+        os.path.join(b.CSRC, f) for f in os.listdir(b.CSRC) if f.endswith(".cu"))
     subprocess.check_call(cmd)
 
 
