@@ -28,6 +28,7 @@
 // the per-column summation order depends only on (K, n, m, plan) -- never on N.
 #pragma once
 #include <cuda.h>
+#include <type_traits>
 #include "common.cuh"
 
 namespace sten {
@@ -431,69 +432,83 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
                     imis[q] = int(gbase[sub0 + q] & 3);
                 }
                 const unsigned char* vbase = sV(buf) + size_t(sub0) * RG * KU * sizeof(TAB);
-                const bool fast = n_divides_ku && ks % KU == 0;
-                for (int kg = 0; kg < nkg; ++kg) {
-                    const unsigned char* vg = vbase + size_t(kg) * BM * KU * sizeof(TAB);
+                // The k-loop, specialised on the addressing mode.  Every staged-row address already
+                // includes this lane's byte offset.  FAST (n | KU, full slab): slot t of k-step kg lies
+                // in block kg KU / n + t / n, so its row address is base_t[t] + idx_byte(t) ROWB with
+                // base_t advanced by one k-step per iteration -- a byte permute and a shift-add per
+                // kept k.  Otherwise: block b = kk / n by multiply-shift, padded slots read a zero row.
+                auto kloop = [&](auto fast_tag) {
+                    constexpr bool FAST = decltype(fast_tag)::value;
+                    uint32_t base_t[KU];
 #pragma unroll
-                    for (int q = 0; q < SUB; ++q) {
-                        int offs[KU];
-                        {
-                            const int o = imis[q] + kg * KU;
-                            const uint32_t wa = iaddr[q] + uint32_t(o & ~3);
-                            const uint32_t x = __funnelshift_r(lds32_addr(wa), lds32_addr(wa + 4u), uint32_t(o & 3) * 8u);
-                            if (fast) {
-                                // n | KU and a full slab: block of slot t = kg KU / n + t / n, no padding
-                                const int rowbase = int(bbase) + kg * kstep_bytes;
+                    for (int t = 0; t < KU; ++t) base_t[t] = bbase + lane_off + uint32_t(tb[t]);
+                    for (int kg = 0; kg < nkg; ++kg) {
+                        const unsigned char* vg = vbase + size_t(kg) * BM * KU * sizeof(TAB);
 #pragma unroll
-                                for (int t = 0; t < KU; ++t)
-                                    offs[t] = rowbase + tb[t] + int((x >> (8 * t)) & 0xffu) * ROWB;
-                            } else {
+                        for (int q = 0; q < SUB; ++q) {
+                            uint32_t offs[KU];
+                            {
+                                const int o = imis[q] + kg * KU;
+                                const uint32_t wa = iaddr[q] + uint32_t(o & ~3);
+                                const uint32_t x =
+                                    __funnelshift_r(lds32_addr(wa), lds32_addr(wa + 4u), uint32_t(o & 3) * 8u);
+                                if constexpr (FAST) {
 #pragma unroll
-                                for (int t = 0; t < KU; ++t) {
-                                    const int kk = kg * KU + t;
-                                    const int b = int((uint32_t(kk) * inv_n) >> 16);
-                                    const int j = int((x >> (8 * t)) & 0xffu);
-                                    offs[t] = kk < ks ? int(bbase) + (b * m + j) * ROWB : int(zero_row);
+                                    for (int t = 0; t < KU; ++t)
+                                        offs[t] = base_t[t] + __byte_perm(x, 0u, 0x4440u + uint32_t(t)) * uint32_t(ROWB);
+                                } else {
+#pragma unroll
+                                    for (int t = 0; t < KU; ++t) {
+                                        const int kk = kg * KU + t;
+                                        const int b = int((uint32_t(kk) * inv_n) >> 16);
+                                        const int j = int((x >> (8 * t)) & 0xffu);
+                                        offs[t] = (kk < ks ? bbase + uint32_t((b * m + j) * ROWB) : zero_row) + lane_off;
+                                    }
+                                }
+                            }
+                            float v[RG][KU];
+#pragma unroll
+                            for (int r = 0; r < RG; ++r) {
+                                const unsigned char* vp = vg + size_t(q * RG + r) * KU * sizeof(TAB);
+                                if constexpr (sizeof(TAB) == 4 && KU == 4) {
+                                    const float4 t = *reinterpret_cast<const float4*>(vp);
+                                    v[r][0] = t.x; v[r][1] = t.y; v[r][2] = t.z; v[r][3] = t.w;
+                                } else if constexpr (sizeof(TAB) == 4) {
+                                    const float2 t = *reinterpret_cast<const float2*>(vp);
+                                    v[r][0] = t.x; v[r][1] = t.y;
+                                } else if constexpr (KU == 4) {
+                                    const uint2 t = *reinterpret_cast<const uint2*>(vp);
+                                    v[r][0] = __uint_as_float(t.x << 16); v[r][1] = __uint_as_float(t.x & 0xffff0000u);
+                                    v[r][2] = __uint_as_float(t.y << 16); v[r][3] = __uint_as_float(t.y & 0xffff0000u);
+                                } else {
+                                    const uint32_t t = *reinterpret_cast<const uint32_t*>(vp);
+                                    v[r][0] = __uint_as_float(t << 16); v[r][1] = __uint_as_float(t & 0xffff0000u);
+                                }
+                            }
+#pragma unroll
+                            for (int t = 0; t < KU; ++t) {
+#pragma unroll
+                                for (int j = 0; j < Cfg::kChunks; ++j) {
+                                    float b[EV];
+                                    unpack<EV>(lds128_addr(offs[t] + uint32_t(j) * 512u), b);
+#pragma unroll
+                                    for (int r = 0; r < RG; ++r)
+#pragma unroll
+                                        for (int e = 0; e < EV; e += 2) {
+                                            float2& c2 = *reinterpret_cast<float2*>(&acc[q][r][j * EV + e]);
+                                            c2 = __ffma2_rn(make_float2(v[r][t], v[r][t]), make_float2(b[e], b[e + 1]), c2);
+                                        }
                                 }
                             }
                         }
-                        float v[RG][KU];
+                        if constexpr (FAST) {
 #pragma unroll
-                        for (int r = 0; r < RG; ++r) {
-                            const unsigned char* vp = vg + size_t(q * RG + r) * KU * sizeof(TAB);
-                            if constexpr (sizeof(TAB) == 4 && KU == 4) {
-                                const float4 t = *reinterpret_cast<const float4*>(vp);
-                                v[r][0] = t.x; v[r][1] = t.y; v[r][2] = t.z; v[r][3] = t.w;
-                            } else if constexpr (sizeof(TAB) == 4) {
-                                const float2 t = *reinterpret_cast<const float2*>(vp);
-                                v[r][0] = t.x; v[r][1] = t.y;
-                            } else if constexpr (KU == 4) {
-                                const uint2 t = *reinterpret_cast<const uint2*>(vp);
-                                v[r][0] = __uint_as_float(t.x << 16); v[r][1] = __uint_as_float(t.x & 0xffff0000u);
-                                v[r][2] = __uint_as_float(t.y << 16); v[r][3] = __uint_as_float(t.y & 0xffff0000u);
-                            } else {
-                                const uint32_t t = *reinterpret_cast<const uint32_t*>(vp);
-                                v[r][0] = __uint_as_float(t << 16); v[r][1] = __uint_as_float(t & 0xffff0000u);
-                            }
-                        }
-#pragma unroll
-                        for (int t = 0; t < KU; ++t) {
-                            const uint32_t ba = uint32_t(offs[t]) + lane_off;
-#pragma unroll
-                            for (int j = 0; j < Cfg::kChunks; ++j) {
-                                float b[EV];
-                                unpack<EV>(lds128_addr(ba + uint32_t(j) * 512u), b);
-#pragma unroll
-                                for (int r = 0; r < RG; ++r)
-#pragma unroll
-                                    for (int e = 0; e < EV; e += 2) {
-                                        float2& c2 = *reinterpret_cast<float2*>(&acc[q][r][j * EV + e]);
-                                        c2 = __ffma2_rn(make_float2(v[r][t], v[r][t]), make_float2(b[e], b[e + 1]), c2);
-                                    }
-                            }
+                            for (int t = 0; t < KU; ++t) base_t[t] += uint32_t(kstep_bytes);
                         }
                     }
-                }
+                };
+                if (n_divides_ku && ks % KU == 0) kloop(std::true_type{});
+                else kloop(std::false_type{});
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[buf]);
