@@ -325,7 +325,7 @@ nmg_spmm_kernel(const NmgSpmmArgs a) {
                 const TAB* vp = sV + size_t(cl) * L * NN;
 #pragma unroll
                 for (int p = 0; p < CP; ++p) {
-#pragma unroll 2
+#pragma unroll 4
                     for (int j = 0; j < g; ++j) {
                         const int s = p * g + j;
                         const uint32_t addr = sBc + uint32_t(ip[s]) * uint32_t(ROWB);

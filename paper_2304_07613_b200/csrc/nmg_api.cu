@@ -41,6 +41,8 @@ sten_status launch_nmg_spmm(const NmgSpmmArgs& a0, cudaStream_t st) {
     const size_t tile = size_t(kNmgSpmmWarps) * MM * kNmgBN * 4;    // split-K partial tile (fp32)
     const int64_t gx = (a.N + kNmgBN - 1) / kNmgBN, gy = (a.RB + kNmgSpmmWarps - 1) / kNmgSpmmWarps;
     // split-K (cluster z) until about two CTAs per SM: S <= 8 (portable cluster), <= chunks
+    // (measured on the C2 shapes: the smallest S reaching two CTAs per SM beats both the largest
+    // one-wave S and ~4 CTAs per SM)
     int S = 1;
     while (S < 8 && gx * gy * S < 2 * 148 && a.NC >= 2 * (S + 1)) ++S;
     a.split = S;
