@@ -127,6 +127,22 @@ sten_status sten_spmm_grouped_nm(sten_nmg f, sten_dtype ab_dt,
                                  const void* B, int64_t ldb, int64_t N,
                                  void* C, int64_t ldc, sten_dtype c_dt, void* stream);
 
+/* SpMM with the all-gather of C fused into the epilogue (token sharding):
+ * this rank computes C_loc = densify(values, idx) x B for its N token columns and the kernel's
+ * epilogue stores every C tile straight into each of the `npeers` gathered output buffers
+ * C_peers[p] ([M][ldc], c_dt; peer-mapped device pointers -- CUDA IPC / symmetric memory over
+ * NVLink, or local buffers) at columns [col0, col0 + N): one kernel does the product and the
+ * exchange, the transfer overlapping the math tile by tile.  C_peers is a HOST array of
+ * 1..8 device pointers.  Completion on the other ranks needs a cross-rank barrier after the
+ * kernel (the caller's).  The fused epilogue is the SIMT kernel's (plan NULL / AUTO -> SIMT;
+ * another algo -> STEN_ERR_UNSUPPORTED); the column order of the sum does not depend on N, so
+ * the gathered buffer equals the single-GPU product bit for bit with the global plan. */
+sten_status sten_spmm_grouped_nm_allgather(sten_nmg f, sten_dtype ab_dt,
+                                           const void* values, const uint8_t* idx, int64_t M, int64_t K,
+                                           const void* B, int64_t ldb, int64_t N,
+                                           void* const* C_peers, int32_t npeers, int64_t col0, int64_t ldc,
+                                           sten_dtype c_dt, const sten_spmm_plan* plan, void* stream);
+
 /* The plan sten_spmm_grouped_nm would use for this problem. */
 sten_status sten_spmm_plan_query(sten_nmg f, sten_dtype ab_dt, int64_t M, int64_t K, int64_t N,
                                  sten_dtype c_dt, sten_spmm_plan* plan);

@@ -76,6 +76,8 @@ __device__ long long g_sten_tl2[256][8];
 #define STEN_WACC(i, t0_) do { } while (0)
 #endif
 
+constexpr int kMaxPeers = 8;    // NVLink domain of one 8-GPU box
+
 // Arguments common to the SpMM kernels.
 struct SpmmArgs {
     const void* values;
@@ -94,7 +96,17 @@ struct SpmmArgs {
     bool v_async;          // else: values rows vector-aligned -> 16B (fp32) / 8B (bf16) cp.async
     int64_t idx_bytes;     // size of the idx array (bounds the aligned-down idx word loads)
     int bperm;             // tcgen05 path: staged-row permutation of the B slab (tc_staged_row)
+    // fused all-gather epilogue (sten_spmm_grouped_nm_allgather): npeer > 0 -> the tile is stored to
+    // every C_peer[p] (peer-mapped [M][ldc] buffers, already offset to this rank's first column)
+    int npeer;
+    void* C_peer[kMaxPeers];
 };
+
+// destination p of the epilogue: C itself, or peer buffer p of the fused all-gather
+template <typename TC>
+STEN_DEVICE_INLINE TC* out_ptr(const SpmmArgs& a, int p) {
+    return static_cast<TC*>(a.npeer ? a.C_peer[p] : a.C);
+}
 
 // WARPS = warps per CTA: WARPS-1 consumer warps + 1 producer warp.
 template <typename TAB, int RG, int TN, int SUB, int WARPS>
@@ -248,7 +260,7 @@ STEN_DEVICE_INLINE void cluster_reduce_store(unsigned char* tile_smem, const Spm
     constexpr int E4 = BM * BN / 4;
     const int e_begin = int(uint64_t(E4) * me / S), e_end = int(uint64_t(E4) * (me + 1) / S);
     const uint32_t base = smem_u32(tile_smem);
-    TC* C = static_cast<TC*>(a.C);
+    const int np = a.npeer ? a.npeer : 1;
     for (int e = e_begin + int(threadIdx.x); e < e_end; e += NT) {
         const uint32_t off = uint32_t(e) * 16u;
         float4 s = ld_dsmem128(map_cluster(base + off, 0));
@@ -261,7 +273,7 @@ STEN_DEVICE_INLINE void cluster_reduce_store(unsigned char* tile_smem, const Spm
         const int64_t gr = m0 + row, gc = n0 + col;
         if (gr < a.M && gc < a.N) {
             const float v[4] = {s.x, s.y, s.z, s.w};
-            store_out<TC>(C, a.ldc, gr, gc, a.N, v, 4, a.c_vec);
+            for (int p = 0; p < np; ++p) store_out<TC>(out_ptr<TC>(a, p), a.ldc, gr, gc, a.N, v, 4, a.c_vec);
         }
     }
     cluster_sync_all();                     // keep every partial alive until all reads are done
@@ -516,18 +528,21 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
         STEN_TSTAMP(3);
         if (a.split == 1) {
             if (!warp_active) return;
-            TC* C = static_cast<TC*>(a.C);
+            const int np = a.npeer ? a.npeer : 1;
+            for (int p = 0; p < np; ++p) {
+                TC* C = out_ptr<TC>(a, p);
 #pragma unroll
-            for (int q = 0; q < SUB; ++q)
+                for (int q = 0; q < SUB; ++q)
 #pragma unroll
-                for (int r = 0; r < RG; ++r) {
-                    const int64_t row = m0 + int64_t(sub0 + q) * RG + r;
-                    if (row >= a.M) continue;
+                    for (int r = 0; r < RG; ++r) {
+                        const int64_t row = m0 + int64_t(sub0 + q) * RG + r;
+                        if (row >= a.M) continue;
 #pragma unroll
-                    for (int j = 0; j < Cfg::kChunks; ++j)
-                        store_out<TC>(C, a.ldc, row, n0 + int64_t(j) * 32 * EV + lane * EV, a.N, &acc[q][r][j * EV],
-                                      EV, a.c_vec);
-                }
+                        for (int j = 0; j < Cfg::kChunks; ++j)
+                            store_out<TC>(C, a.ldc, row, n0 + int64_t(j) * 32 * EV + lane * EV, a.N,
+                                          &acc[q][r][j * EV], EV, a.c_vec);
+                    }
+            }
             return;
         }
     }

@@ -169,3 +169,44 @@ class RowShardedSpmm:
         else:
             gathered.copy_(local)
         return torch.cat([gathered[p * maxr: p * maxr + (r1 - r0)] for p, (r0, r1) in enumerate(rows)], dim=0)
+
+
+class FusedAllGatherSpmm:
+    """Token sharding with the all-gather fused into the SpMM epilogue over NVLink peer memory.
+
+    The gathered output C [M][N_pad] lives in symmetric memory (one allocation per rank,
+    mapped into every peer: ``torch.distributed._symmetric_memory``); each rank's kernel
+    (``sten_spmm_grouped_nm_allgather``) stores its C tiles straight into the slot
+    [p * n_local, (p + 1) * n_local) of EVERY rank's buffer, so the exchange overlaps the
+    math tile by tile and no NCCL call runs; a device-side barrier over the symmetric
+    memory handle ends the step.  Needs one GPU per rank with peer access (NVLink /
+    NVSwitch); the kernel path itself is tested on one GPU with local stand-in buffers
+    (tests/test_gpu_parity.py::test_spmm_fused_allgather_equals_unsharded).
+    """
+
+    def __init__(self, values, idx, n, m, g, K, N_global, out_dtype=None, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        from . import sten
+        self.values, self.idx, self.n, self.m, self.g = values, idx, n, m, g
+        self.M = values.shape[0]
+        self.out_dtype = out_dtype or values.dtype
+        self.group = group or dist.group.WORLD
+        self.world, self.rank = _world(self.group)
+        self.N_global = N_global
+        self.n_local = padded_shard_width(N_global, self.world)
+        # the GLOBAL plan (pin P11), restricted to the fused-epilogue kernel (SIMT)
+        plan = sten.spmm_plan(n, m, g, self.M, K, N_global, ab_dtype=values.dtype, c_dtype=self.out_dtype)
+        plan.algo = sten.ALGO_SIMT if plan.algo != sten.ALGO_SIMT else plan.algo
+        self.plan = plan
+        ldc = self.world * self.n_local
+        self.buf = symm_mem.empty((self.M, ldc), dtype=self.out_dtype, device=values.device)
+        self.handle = symm_mem.rendezvous(self.buf, self.group)
+        self.peers = [self.handle.get_buffer(p, (self.M, ldc), self.out_dtype) for p in range(self.world)]
+
+    def forward(self, B_local: torch.Tensor) -> torch.Tensor:
+        """C [M][N_global] on every rank; B_local = this rank's columns of B."""
+        from . import sten
+        sten.spmm_grouped_nm_allgather(self.values, self.idx, B_local, self.n, self.m, self.g, self.peers,
+                                       self.rank * self.n_local, plan=self.plan)
+        self.handle.barrier(channel=0)          # every peer's stores into this buffer have landed
+        return self.buf[:, : self.N_global]

@@ -68,6 +68,10 @@ SIGNATURES = {
                                                      _i64, _vp, _i64, ctypes.c_int, _vp, _i64, _vp]),
     "sten_resparsify_same_format": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _vp,
                                                    _vp]),
+    "sten_spmm_grouped_nm_allgather": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64,
+                                                      _i64, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
+                                                      _i64, _i64, ctypes.c_int, ctypes.POINTER(sten_spmm_plan),
+                                                      _vp]),
     "sten_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "sten_algo_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "sten_spmm_launch_count": (ctypes.c_int32, [ctypes.POINTER(sten_spmm_plan)]),
@@ -223,6 +227,25 @@ def spmm_autotune(values: torch.Tensor, idx: torch.Tensor, B: torch.Tensor, n: i
                                      B.data_ptr(), _ld(B), N, out.data_ptr(), _ld(out), _dt(out), int(reps),
                                      _stream(stream), ctypes.byref(plan)), "sten_spmm_autotune")
     return plan
+
+
+def spmm_grouped_nm_allgather(values: torch.Tensor, idx: torch.Tensor, B: torch.Tensor, n: int, m: int, g: int,
+                              outs, col0: int, plan: sten_spmm_plan | None = None, stream=None):
+    """C_loc = densify(values, idx) @ B written by the SpMM epilogue into columns [col0, col0 + N) of
+    EVERY buffer in `outs` (the gathered [M][ldc] outputs of all ranks: peer-mapped views, or
+    local tensors) -- sten_spmm_grouped_nm_allgather."""
+    _cuda(B, "B")
+    M = values.shape[0]
+    K, N = B.shape
+    ld = _ld(outs[0])
+    if any(_ld(o) != ld or o.dtype != outs[0].dtype or o.shape[0] != M for o in outs):
+        raise ValueError("every gathered output must share shape, ld and dtype")
+    ptrs = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+    _check(load().sten_spmm_grouped_nm_allgather(
+        sten_nmg(n, m, g), _dt(values), values.data_ptr(), idx.data_ptr(), M, K, B.data_ptr(), _ld(B), N,
+        ptrs, len(outs), col0, ld, _dt(outs[0]), ctypes.byref(plan) if plan is not None else None,
+        _stream(stream)), "sten_spmm_grouped_nm_allgather")
+    return outs
 
 
 def sparse_linear_host(W_host: torch.Tensor, B_host: torch.Tensor, n: int, m: int, g: int,

@@ -431,3 +431,43 @@ def test_resparsify_same_format_bit_exact(dtype, n, m, g, ld_multiple):
     _, i_ref = oracle.sparsify(W, n, m, g)
     v2_ref = oracle.same_format(W2, i_ref, n, m, g)
     assert np.array_equal(host(v2).view(np.uint8), v2_ref.view(np.uint8))
+
+
+# ----------------------------------------------------------------------------------------
+# 8(e): SpMM with the all-gather fused into the epilogue (peer buffers; local stand-ins here)
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("split", [1, 3])
+@pytest.mark.parametrize("P", [2, 4])
+def test_spmm_fused_allgather_equals_unsharded(split, P):
+    """P simulated ranks each compute their token shard and push it into all P gathered buffers;
+    every buffer then equals the unsharded product bit for bit (global plan, pin P11)."""
+    n, m, g, M, K, N = 2, 4, 4, 96, 256, 4 * 136
+    W = synthetic.weights(M, K, seed=21)
+    B = synthetic.activations(K, N, seed=22)
+    v, i = gpu_sparsify(W, n, m, g, "f32")
+    Bd = dev(B, "f32")
+    plan = sten.make_plan(sten.ALGO_SIMT, split_k=split, tile=1)
+    C_full = sten.spmm_grouped_nm(v, i, Bd, n, m, g, plan=plan)
+    outs = [torch.full((M, N), float("nan"), device="cuda") for _ in range(P)]
+    per = N // P
+    for r in range(P):                                   # rank r's call
+        sten.spmm_grouped_nm_allgather(v, i, Bd[:, r * per:(r + 1) * per], n, m, g, outs, r * per, plan=plan)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, C_full)
+    with pytest.raises(sten.StenError):                   # the fused epilogue is the SIMT kernel's
+        sten.spmm_grouped_nm_allgather(v, i, Bd[:, :per], n, m, g, outs, 0,
+                                       plan=sten.make_plan(sten.ALGO_MMA_SYNC, 1, 1))
+
+
+def test_fused_allgather_symmetric_memory_world1():
+    """parallel.FusedAllGatherSpmm end to end on a one-rank NCCL group: symmetric-memory
+    rendezvous, peer views, the fused-epilogue SpMM and the device barrier (the 8-GPU case runs
+    the same code with 8 peer views)."""
+    import os, socket, subprocess, sys
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "fused_allgather_w1.py")], cwd=root, env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert "fused world=1 equal: True" in out.stdout, out.stdout + out.stderr
