@@ -143,6 +143,19 @@ sten_status sten_spmm_grouped_nm_allgather(sten_nmg f, sten_dtype ab_dt,
                                            void* const* C_peers, int32_t npeers, int64_t col0, int64_t ldc,
                                            sten_dtype c_dt, const sten_spmm_plan* plan, void* stream);
 
+/* NEXT-3 epilogue fusion (the BERT FFN1 pattern): C = act(densify(values, idx) x B
+ * + bias) computed in the SpMM's fp32 epilogue (after the split-K reduction) before the store.
+ *   bias [M] fp32 device pointer or NULL (bias of output feature r, added to row r of C)
+ *   act  0 = none, 1 = GELU x/2 (1 + erf(x / sqrt 2)), 2 = ReLU; other -> STEN_ERR_INVALID_ARG
+ * The fused epilogue is the SIMT kernel's (plan NULL / AUTO -> SIMT; another algo ->
+ * STEN_ERR_UNSUPPORTED); arguments otherwise as sten_spmm_grouped_nm_ex. */
+sten_status sten_spmm_grouped_nm_bias_act(sten_nmg f, sten_dtype ab_dt,
+                                          const void* values, const uint8_t* idx, int64_t M, int64_t K,
+                                          const void* B, int64_t ldb, int64_t N,
+                                          void* C, int64_t ldc, sten_dtype c_dt,
+                                          const float* bias, int32_t act,
+                                          const sten_spmm_plan* plan, void* stream);
+
 /* The plan sten_spmm_grouped_nm would use for this problem. */
 sten_status sten_spmm_plan_query(sten_nmg f, sten_dtype ab_dt, int64_t M, int64_t K, int64_t N,
                                  sten_dtype c_dt, sten_spmm_plan* plan);

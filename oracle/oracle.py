@@ -276,3 +276,25 @@ def same_format(W: np.ndarray, idx: np.ndarray, n: int, m: int, g: int) -> np.nd
     _check(_load().oracle_same_format(n, m, g, _dtype_code(W), _p(W), M, K, K, _p(idx), _p(values)),
            "same_format")
     return values
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-3 epilogue (bias + activation of a BERT linear), fp64
+# ---------------------------------------------------------------------------------------------
+def gelu(x: np.ndarray) -> np.ndarray:
+    """GELU, erf form: x/2 (1 + erf(x / sqrt 2)) in fp64 (math.erf per element; small inputs)."""
+    import math
+    f = np.frompyfunc(lambda t: 0.5 * t * (1.0 + math.erf(t / math.sqrt(2.0))), 1, 1)
+    return f(np.asarray(x, dtype=np.float64)).astype(np.float64)
+
+
+def bias_act(C: np.ndarray, bias: np.ndarray | None, act: int) -> np.ndarray:
+    """act(C + bias[:, None]) in fp64; act 0 none, 1 GELU, 2 ReLU."""
+    y = np.asarray(C, dtype=np.float64)
+    if bias is not None:
+        y = y + np.asarray(bias, dtype=np.float64)[:, None]
+    if act == 1:
+        y = gelu(y)
+    elif act == 2:
+        y = np.maximum(y, 0.0)
+    return y

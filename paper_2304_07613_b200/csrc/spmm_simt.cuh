@@ -100,7 +100,23 @@ struct SpmmArgs {
     // every C_peer[p] (peer-mapped [M][ldc] buffers, already offset to this rank's first column)
     int npeer;
     void* C_peer[kMaxPeers];
+    // fused epilogue (sten_spmm_grouped_nm_bias_act): C = act(C + bias[row]) before the store
+    const float* bias;     // [M] or NULL
+    int act;               // 0 none, 1 GELU (erf form), 2 ReLU
 };
+
+// the fused epilogue on the fp32 accumulators of one output row (NEXT-3: "bias + GELU ...
+// epilogue fusion into the SpMM"); GELU(x) = x/2 (1 + erf(x / sqrt 2))
+STEN_DEVICE_INLINE void epilogue(const SpmmArgs& a, int64_t row, float* v, int cnt) {
+    if (!a.bias && a.act == 0) return;
+    const float b = a.bias ? a.bias[row] : 0.0f;
+    for (int e = 0; e < cnt; ++e) {
+        float x = v[e] + b;
+        if (a.act == 1) x = 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+        else if (a.act == 2) x = fmaxf(x, 0.0f);
+        v[e] = x;
+    }
+}
 
 // destination p of the epilogue: C itself, or peer buffer p of the fused all-gather
 template <typename TC>
@@ -272,7 +288,8 @@ STEN_DEVICE_INLINE void cluster_reduce_store(unsigned char* tile_smem, const Spm
         const int row = (e * 4) / BN, col = (e * 4) % BN;
         const int64_t gr = m0 + row, gc = n0 + col;
         if (gr < a.M && gc < a.N) {
-            const float v[4] = {s.x, s.y, s.z, s.w};
+            float v[4] = {s.x, s.y, s.z, s.w};
+            epilogue(a, gr, v, 4);
             for (int p = 0; p < np; ++p) store_out<TC>(out_ptr<TC>(a, p), a.ldc, gr, gc, a.N, v, 4, a.c_vec);
         }
     }
@@ -528,6 +545,15 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
         STEN_TSTAMP(3);
         if (a.split == 1) {
             if (!warp_active) return;
+            if (a.bias || a.act) {
+#pragma unroll
+                for (int q = 0; q < SUB; ++q)
+#pragma unroll
+                    for (int r = 0; r < RG; ++r) {
+                        const int64_t row = m0 + int64_t(sub0 + q) * RG + r;
+                        if (row < a.M) epilogue(a, row, acc[q][r], TN);
+                    }
+            }
             const int np = a.npeer ? a.npeer : 1;
             for (int p = 0; p < np; ++p) {
                 TC* C = out_ptr<TC>(a, p);

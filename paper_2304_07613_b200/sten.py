@@ -72,6 +72,9 @@ SIGNATURES = {
                                                       _i64, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32,
                                                       _i64, _i64, ctypes.c_int, ctypes.POINTER(sten_spmm_plan),
                                                       _vp]),
+    "sten_spmm_grouped_nm_bias_act": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64,
+                                                     _i64, _vp, _i64, ctypes.c_int, _vp, ctypes.c_int32,
+                                                     ctypes.POINTER(sten_spmm_plan), _vp]),
     "sten_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "sten_algo_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "sten_spmm_launch_count": (ctypes.c_int32, [ctypes.POINTER(sten_spmm_plan)]),
@@ -246,6 +249,27 @@ def spmm_grouped_nm_allgather(values: torch.Tensor, idx: torch.Tensor, B: torch.
         ptrs, len(outs), col0, ld, _dt(outs[0]), ctypes.byref(plan) if plan is not None else None,
         _stream(stream)), "sten_spmm_grouped_nm_allgather")
     return outs
+
+
+ACT_NONE, ACT_GELU, ACT_RELU = 0, 1, 2
+
+
+def spmm_grouped_nm_bias_act(values: torch.Tensor, idx: torch.Tensor, B: torch.Tensor, n: int, m: int, g: int,
+                             bias: torch.Tensor | None = None, act: int = ACT_GELU, out: torch.Tensor | None = None,
+                             out_dtype=None, plan: sten_spmm_plan | None = None, stream=None) -> torch.Tensor:
+    """C = act(densify(values, idx) @ B + bias[:, None]) with the bias/activation in the SpMM epilogue."""
+    _cuda(B, "B")
+    M = values.shape[0]
+    K, N = B.shape
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype or values.dtype, device=B.device)
+    if bias is not None and (bias.dtype != torch.float32 or bias.numel() != M or not bias.is_contiguous()):
+        raise ValueError("bias must be a contiguous float32 vector of length M")
+    _check(load().sten_spmm_grouped_nm_bias_act(
+        sten_nmg(n, m, g), _dt(values), values.data_ptr(), idx.data_ptr(), M, K, B.data_ptr(), _ld(B), N,
+        out.data_ptr(), _ld(out), _dt(out), bias.data_ptr() if bias is not None else None, act,
+        ctypes.byref(plan) if plan is not None else None, _stream(stream)), "sten_spmm_grouped_nm_bias_act")
+    return out
 
 
 def sparse_linear_host(W_host: torch.Tensor, B_host: torch.Tensor, n: int, m: int, g: int,

@@ -471,3 +471,28 @@ def test_fused_allgather_symmetric_memory_world1():
     out = subprocess.run([sys.executable, os.path.join(root, "tools", "fused_allgather_w1.py")], cwd=root, env=env,
                          capture_output=True, text=True, timeout=300)
     assert "fused world=1 equal: True" in out.stdout, out.stdout + out.stderr
+
+
+# ----------------------------------------------------------------------------------------
+# NEXT-3: bias + activation fused into the SpMM epilogue
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("act", [0, 1, 2])
+@pytest.mark.parametrize("split", [1, 4])
+@pytest.mark.parametrize("with_bias", [True, False])
+def test_spmm_bias_act_epilogue(act, split, with_bias):
+    n, m, g, M, K, N = 2, 4, 4, 120, 384, 200
+    W = synthetic.weights(M, K, seed=31)
+    B = synthetic.activations(K, N, seed=32)
+    bias = (np.random.default_rng(33).standard_normal(M) * 0.1).astype(np.float32)
+    v, i = gpu_sparsify(W, n, m, g, "f32")
+    plan = sten.make_plan(sten.ALGO_SIMT, split_k=split, tile=1)
+    C = sten.spmm_grouped_nm_bias_act(v, i, dev(B, "f32"), n, m, g,
+                                      bias=torch.from_numpy(bias).cuda() if with_bias else None, act=act, plan=plan)
+    torch.cuda.synchronize()
+    v_ref, i_ref = oracle.sparsify(W, n, m, g)
+    C_ref, Bound = oracle.spmm(v_ref, i_ref, B, n, m, g)
+    Y = oracle.bias_act(C_ref, bias if with_bias else None, act)
+    # |act(c) - act(c_ref)| <= 1.13 |c - c_ref| (GELU' <= 1.13), plus fp32 rounding of the bias add
+    # and erff (a few ulp of the result)
+    tol = 1.13 * 1e-5 * Bound + 4e-7 * np.abs(Y) + 1e-7 * (np.abs(C_ref) + (np.abs(bias)[:, None] if with_bias else 0))
+    assert (np.abs(C.cpu().numpy().astype(np.float64) - Y) <= tol + 1e-30).all()

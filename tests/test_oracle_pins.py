@@ -298,3 +298,20 @@ def test_same_format_pins(n, m, g):
     Wb = synthetic.weights(6 * g, 5 * m, seed=7, dtype="bf16")
     vb, ib = oracle.sparsify(Wb, n, m, g)
     assert np.array_equal(oracle.same_format(Wb, ib, n, m, g), vb)
+
+
+# ----------------------------------------------------------------------------------------
+# NEXT-3 epilogue: GELU / bias / ReLU closed forms
+# ----------------------------------------------------------------------------------------
+def test_gelu_bias_act_pins():
+    x = np.array([-3.0, -1.0, 0.0, 1.0, 2.5, 40.0])
+    y = oracle.gelu(x)
+    assert y[2] == 0.0
+    assert abs(y[3] - 0.8413447460685429) < 1e-15            # GELU(1) = Phi(1)
+    assert abs(y[5] - 40.0) < 1e-12                          # -> x for large x
+    assert np.allclose(oracle.gelu(-x), y - x, rtol=0, atol=1e-15)   # GELU(-x) = GELU(x) - x (erf odd)
+    C = np.array([[1.0, -2.0], [0.5, 0.0]])
+    b = np.array([0.5, -1.0])
+    assert np.array_equal(oracle.bias_act(C, b, 0), C + b[:, None])
+    assert np.array_equal(oracle.bias_act(C, b, 2), np.maximum(C + b[:, None], 0))
+    assert np.allclose(oracle.bias_act(C, None, 1), oracle.gelu(C))
