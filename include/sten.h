@@ -156,6 +156,27 @@ sten_status sten_spmm_grouped_nm_bias_act(sten_nmg f, sten_dtype ab_dt,
                                           const float* bias, int32_t act,
                                           const sten_spmm_plan* plan, void* stream);
 
+/* Grouped launch of independent fp32 problems (e.g. the linears of a step): ONE kernel launch
+ * whose CTAs each run one whole-K output tile of one problem (cuBLAS-grouped-GEMM style; no
+ * split-K, no cluster), the problems ordered longest-K first.  Every problem: fp32 values / B /
+ * C, arguments and layout as sten_spmm_grouped_nm; all problems must map to the same SIMT
+ * variant (the same row-group class: g % 8 == 0, g % 4 == 0, g % 2 == 0 or odd) else
+ * STEN_ERR_UNSUPPORTED.  count in 1..12; tile 0/1 (8 warps, 56 x 256) or 2 (16 warps,
+ * 120 x 256).  Results equal sten_spmm_grouped_nm_ex with the same tile and split_k = 1. */
+typedef struct {
+    sten_nmg f;
+    int32_t reserved;
+    const void* values;
+    const uint8_t* idx;
+    int64_t M, K;
+    const void* B;
+    int64_t ldb, N;
+    void* C;
+    int64_t ldc;
+} sten_spmm_problem;
+sten_status sten_spmm_grouped_nm_batched(int32_t count, const sten_spmm_problem* problems, int32_t tile,
+                                         void* stream);
+
 /* The plan sten_spmm_grouped_nm would use for this problem. */
 sten_status sten_spmm_plan_query(sten_nmg f, sten_dtype ab_dt, int64_t M, int64_t K, int64_t N,
                                  sten_dtype c_dt, sten_spmm_plan* plan);

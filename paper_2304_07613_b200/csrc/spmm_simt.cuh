@@ -306,8 +306,8 @@ STEN_DEVICE_INLINE void cluster_reduce_store(unsigned char* tile_smem, const Spm
 // addresses of staged B rows (warp-private), runs the LDS/FFMA2 loop and arrives on
 // the empty barrier.  No CTA-wide barrier per slab.
 template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS, int MINB>
-__global__ void __launch_bounds__(WARPS * 32, MINB)
-spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmV) {
+__device__ __forceinline__ void spmm_simt_body(const SpmmArgs& a, const CUtensorMap* tmB, const CUtensorMap* tmV,
+                                               const int bx, const int by, const int bz) {
     using Cfg = SimtCfg<TAB, RG, TN, SUB, WARPS>;
     constexpr int EV = Cfg::kEV;
     constexpr int BN = Cfg::kBN;
@@ -329,13 +329,13 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int64_t n0 = int64_t(blockIdx.x) * BN;
-    const int64_t m0 = int64_t(blockIdx.y) * BM;
+    const int64_t n0 = int64_t(bx) * BN;
+    const int64_t m0 = int64_t(by) * BM;
     // split-K part z = blockIdx.z owns slabs [z T / S, (z+1) T / S) of the T slabs (balanced: the
     // parts differ by at most one slab, so no CTA of the cluster idles at the reduction barrier)
     const int64_t tot_slabs = (a.KB + kbs - 1) / kbs;
-    const int64_t kb_begin = (tot_slabs * int64_t(blockIdx.z) / a.split) * kbs;
-    const int64_t kb_end = min64(a.KB, (tot_slabs * int64_t(blockIdx.z + 1) / a.split) * kbs);
+    const int64_t kb_begin = (tot_slabs * int64_t(bz) / a.split) * kbs;
+    const int64_t kb_end = min64(a.KB, (tot_slabs * int64_t(bz + 1) / a.split) * kbs);
     const int nslabs = kb_end > kb_begin ? int((kb_end - kb_begin + kbs - 1) / kbs) : 0;
 
     auto sB = [&](int buf) { return smem + L.stages + size_t(buf) * L.stage; };
@@ -381,8 +381,8 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
             if (lane == 0) {
                 fence_proxy_async_smem();
                 mbar_expect_tx(&full[buf], tx_bytes);
-                tma_load_2d(sB(buf), &tmB, &full[buf], int(n0), int(kb0 * m));
-                if (a.v_tma) tma_load_3d(sV(buf), &tmV, &full[buf], 0, int(m0), int(kb0 * n / KU));
+                tma_load_2d(sB(buf), tmB, &full[buf], int(n0), int(kb0 * m));
+                if (a.v_tma) tma_load_3d(sV(buf), tmV, &full[buf], 0, int(m0), int(kb0 * n / KU));
             }
             if (!a.v_tma) {
                 // values tile in k-group-major layout [ksp/KU][BM][KU] (zero beyond ks and beyond M)
@@ -595,6 +595,39 @@ spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, cons
     STEN_TSTAMP(4);
     cluster_reduce_store<TC, BM, BN, NT>(smem + L.hdr, a, m0, n0);
     STEN_TSTAMP(5);
+}
+
+// one problem per launch: grid (N tiles, M tiles, split-K parts)
+template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
+spmm_simt_kernel(const SpmmArgs a, const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmV) {
+    spmm_simt_body<TAB, TC, RG, TN, SUB, WARPS, MINB>(a, &tmB, &tmV, int(blockIdx.x), int(blockIdx.y),
+                                                       int(blockIdx.z));
+}
+
+// Grouped launch of independent problems (the cases of a step; cuBLAS-grouped-GEMM style): CTA b
+// runs tile (b - tile0[p]) of problem p, row-tile-major, whole K (no split-K, no cluster).  The
+// problems share the kernel variant (dtypes, RG, tile); the list is ordered longest-K first on
+// the host so the block scheduler fills the tail with short tiles.
+constexpr int kMaxBatch = 12;
+struct SpmmBatch {
+    SpmmArgs a[kMaxBatch];
+    CUtensorMap tmB[kMaxBatch];
+    CUtensorMap tmV[kMaxBatch];
+    int tile0[kMaxBatch + 1];    // first CTA of each problem; tile0[count] = grid size
+    int ntx[kMaxBatch];          // N tiles of each problem
+    int count;
+};
+
+template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
+spmm_simt_batched_kernel(const __grid_constant__ SpmmBatch bt) {
+    const int b = int(blockIdx.x);
+    int p = 0;
+    while (p + 1 < bt.count && b >= bt.tile0[p + 1]) ++p;
+    const int t = b - bt.tile0[p];
+    spmm_simt_body<TAB, TC, RG, TN, SUB, WARPS, MINB>(bt.a[p], &bt.tmB[p], &bt.tmV[p], t % bt.ntx[p],
+                                                       t / bt.ntx[p], 0);
 }
 
 }  // namespace sten

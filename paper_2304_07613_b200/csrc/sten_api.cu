@@ -171,24 +171,36 @@ int simt_slab_blocks(sten_nmg f, sten_dtype ab, int tile) {
     return best;
 }
 
-template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS, int MINB = (WARPS == 8 ? 2 : 1)>
-sten_status launch_simt_cfg(SpmmArgs a, cudaStream_t st) {
+// tensor maps of one SIMT problem (B slab box, values box) and its shared-memory size
+template <typename TAB, int RG, int TN, int SUB, int WARPS>
+sten_status prep_simt(SpmmArgs& a, CUtensorMap* tmB, CUtensorMap* tmV, size_t* smem) {
     using Cfg = SimtCfg<TAB, RG, TN, SUB, WARPS>;
     const SimtSmem<TAB, RG, TN, SUB, WARPS> L(a.kbs, a.n, a.m);
     if (L.total > 227 * 1024) return STEN_ERR_UNSUPPORTED;
     const CUtensorMapDataType tdt = sizeof(TAB) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     constexpr size_t s = sizeof(TAB);
-    CUtensorMap tmB, tmV;
-    memset(&tmB, 0, sizeof(tmB));
-    memset(&tmV, 0, sizeof(tmV));
-    if (!make_tmap_2d(&tmB, a.B, tdt, uint64_t(a.N), uint64_t(a.K), uint64_t(a.ldb) * s, Cfg::kBN, uint32_t(L.bk)))
+    memset(tmB, 0, sizeof(*tmB));
+    memset(tmV, 0, sizeof(*tmV));
+    if (!make_tmap_2d(tmB, a.B, tdt, uint64_t(a.N), uint64_t(a.K), uint64_t(a.ldb) * s, Cfg::kBN, uint32_t(L.bk)))
         return STEN_ERR_CUDA;
     // values as a 3-D tensor {KU, M, Kp/KU} (strides Kp*s, KU*s) so the box lands as [ksp/KU][BM][KU];
     // needs 16-byte inner boxes and strides, else the kernel stages values with cp.async
     constexpr int KU = Cfg::kKU;
     a.v_tma = KU * s == 16 && (size_t(a.Kp) * s) % 16 == 0 && aligned16(a.values) &&
-              make_tmap_3d(&tmV, a.values, tdt, uint64_t(KU), uint64_t(a.M), uint64_t(a.Kp / KU),
+              make_tmap_3d(tmV, a.values, tdt, uint64_t(KU), uint64_t(a.M), uint64_t(a.Kp / KU),
                            uint64_t(a.Kp) * s, uint64_t(KU) * s, uint32_t(KU), Cfg::kBM, uint32_t(L.ksp / KU));
+    *smem = L.total;
+    return STEN_OK;
+}
+
+template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS, int MINB = (WARPS == 8 ? 2 : 1)>
+sten_status launch_simt_cfg(SpmmArgs a, cudaStream_t st) {
+    using Cfg = SimtCfg<TAB, RG, TN, SUB, WARPS>;
+    CUtensorMap tmB, tmV;
+    size_t smem_bytes = 0;
+    sten_status ps = prep_simt<TAB, RG, TN, SUB, WARPS>(a, &tmB, &tmV, &smem_bytes);
+    if (ps) return ps;
+    struct { size_t total; } L = {smem_bytes};
     auto kern = spmm_simt_kernel<TAB, TC, RG, TN, SUB, WARPS, MINB>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total)) != cudaSuccess)
         return STEN_ERR_CUDA;
@@ -207,6 +219,45 @@ sten_status launch_simt_cfg(SpmmArgs a, cudaStream_t st) {
     cfg.numAttrs = a.split > 1 ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, kern, a, tmB, tmV) != cudaSuccess) return STEN_ERR_CUDA;
     return last_cuda();
+}
+
+// grouped launch of `count` fp32 problems sharing the kernel variant (sten_spmm_grouped_nm_batched)
+template <int RG, int TN, int SUB, int WARPS, int MINB = (WARPS == 8 ? 2 : 1)>
+sten_status launch_simt_batch_cfg(SpmmArgs* as, int count, cudaStream_t st) {
+    using Cfg = SimtCfg<float, RG, TN, SUB, WARPS>;
+    SpmmBatch bt;                  // the kernel parameter (copied at launch; no library state)
+    memset(&bt, 0, sizeof(bt));
+    size_t smem_max = 0;
+    int tiles = 0;
+    for (int p = 0; p < count; ++p) {
+        size_t sm = 0;
+        sten_status ps = prep_simt<float, RG, TN, SUB, WARPS>(as[p], &bt.tmB[p], &bt.tmV[p], &sm);
+        if (ps) return ps;
+        bt.a[p] = as[p];
+        const int ntx = int((as[p].N + Cfg::kBN - 1) / Cfg::kBN), nty = int((as[p].M + Cfg::kBM - 1) / Cfg::kBM);
+        bt.tile0[p] = tiles;
+        bt.ntx[p] = ntx;
+        tiles += ntx * nty;
+        smem_max = std::max(smem_max, sm);
+    }
+    bt.tile0[count] = tiles;
+    bt.count = count;
+    if (tiles == 0) return STEN_OK;
+    auto kern = spmm_simt_batched_kernel<float, float, RG, TN, SUB, WARPS, MINB>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max)) != cudaSuccess)
+        return STEN_ERR_CUDA;
+    kern<<<unsigned(tiles), Cfg::kThreads, smem_max, st>>>(bt);
+    return last_cuda();
+}
+
+template <int RG>
+sten_status launch_simt_batch_rg(SpmmArgs* as, int count, int tile, cudaStream_t st) {
+    constexpr int SUB8 = 8 / RG;
+    switch (tile) {
+        case 1: return launch_simt_batch_cfg<RG, 8, SUB8, 8>(as, count, st);
+        case 2: return launch_simt_batch_cfg<RG, 8, SUB8, 16>(as, count, st);
+    }
+    return STEN_ERR_UNSUPPORTED;
 }
 
 template <typename TAB, typename TC, int RG>
@@ -487,6 +538,57 @@ sten_status sten_spmm_grouped_nm_bias_act(sten_nmg f, sten_dtype ab_dt, const vo
     if (M > 0 && N > 0 && K == 0) return STEN_ERR_UNSUPPORTED;       // no fused zero-fill path
     return spmm_impl(f, ab_dt, values, idx, M, K, B, ldb, N, C, ldc, c_dt, &pl, as_stream(stream), nullptr, 0, 0,
                      bias, act);
+}
+
+sten_status sten_spmm_grouped_nm_batched(int32_t count, const sten_spmm_problem* probs, int32_t tile,
+                                         void* stream) {
+    if (count < 1 || count > kMaxBatch || !probs) return STEN_ERR_INVALID_ARG;
+    if (tile == 0) tile = 1;
+    if (tile != 1 && tile != 2) return STEN_ERR_UNSUPPORTED;
+    SpmmArgs as[kMaxBatch];
+    int order[kMaxBatch];
+    const int rg = simt_rows_per_warp(probs[0].f.g);
+    for (int p = 0; p < count; ++p) {
+        const sten_spmm_problem& q = probs[p];
+        const sten_nmg f = q.f;
+        sten_status s = check_format(f);
+        if (s) return s;
+        if ((s = check_shape(f, q.M, q.K))) return s;
+        if (q.N < 0 || q.ldb < q.N || q.ldc < q.N) return STEN_ERR_SHAPE;
+        if ((q.M * q.K > 0 && (!q.values || !q.idx)) || (q.K * q.N > 0 && !q.B) || (q.M * q.N > 0 && !q.C))
+            return STEN_ERR_INVALID_ARG;
+        if (simt_rows_per_warp(f.g) != rg) return STEN_ERR_UNSUPPORTED;    // one kernel variant per launch
+        if (q.K == 0 && q.M * q.N > 0) return STEN_ERR_UNSUPPORTED;
+        if (q.K * q.N > 0 && (!aligned16(q.B) || (q.ldb * 4) % 16 != 0)) return STEN_ERR_UNSUPPORTED;
+        if ((reinterpret_cast<uintptr_t>(q.idx) & 3u) != 0) return STEN_ERR_UNSUPPORTED;
+        SpmmArgs& a = as[p];
+        memset(&a, 0, sizeof(a));
+        a.values = q.values; a.idx = q.idx; a.B = q.B; a.C = q.C;
+        a.M = q.M; a.K = q.K; a.N = q.N; a.ldb = q.ldb; a.ldc = q.ldc;
+        a.n = f.n; a.m = f.m; a.g = f.g;
+        a.KB = q.K / f.m; a.Kp = a.KB * f.n;
+        a.c_vec = aligned16(q.C) && (q.ldc * 4) % 16 == 0;
+        a.v_async = (a.Kp % 4 == 0) && ((reinterpret_cast<uintptr_t>(q.values) & 15u) == 0);
+        a.idx_bytes = (q.M / f.g) * a.KB * f.n;
+        a.kbs = simt_slab_blocks(f, STEN_F32, tile);
+        a.split = 1;
+        a.kb_per_split = a.KB;
+        order[p] = p;
+    }
+    // longest K first: the block scheduler then fills the tail with short tiles
+    std::stable_sort(order, order + count, [&](int x, int y) { return as[x].Kp > as[y].Kp; });
+    SpmmArgs sorted[kMaxBatch];
+    int live = 0;
+    for (int p = 0; p < count; ++p)
+        if (as[order[p]].M > 0 && as[order[p]].N > 0) sorted[live++] = as[order[p]];
+    if (live == 0) return STEN_OK;
+    cudaStream_t st = as_stream(stream);
+    switch (rg) {
+        case 8: return launch_simt_batch_rg<8>(sorted, live, tile, st);
+        case 4: return launch_simt_batch_rg<4>(sorted, live, tile, st);
+        case 2: return launch_simt_batch_rg<2>(sorted, live, tile, st);
+        default: return launch_simt_batch_rg<1>(sorted, live, tile, st);
+    }
 }
 
 sten_status sten_resparsify_same_format(sten_nmg f, sten_dtype dt, const void* W, int64_t M, int64_t K,

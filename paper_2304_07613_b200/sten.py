@@ -31,6 +31,12 @@ class sten_nmg(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("m", ctypes.c_int32), ("g", ctypes.c_int32)]
 
 
+class sten_spmm_problem(ctypes.Structure):
+    _fields_ = [("f", sten_nmg), ("reserved", ctypes.c_int32), ("values", ctypes.c_void_p), ("idx", ctypes.c_void_p),
+                ("M", ctypes.c_int64), ("K", ctypes.c_int64), ("B", ctypes.c_void_p), ("ldb", ctypes.c_int64),
+                ("N", ctypes.c_int64), ("C", ctypes.c_void_p), ("ldc", ctypes.c_int64)]
+
+
 class sten_spmm_plan(ctypes.Structure):
     _fields_ = [("algo", ctypes.c_int32), ("split_k", ctypes.c_int32), ("tile", ctypes.c_int32),
                 ("reserved", ctypes.c_int32 * 5)]
@@ -75,6 +81,8 @@ SIGNATURES = {
     "sten_spmm_grouped_nm_bias_act": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64,
                                                      _i64, _vp, _i64, ctypes.c_int, _vp, ctypes.c_int32,
                                                      ctypes.POINTER(sten_spmm_plan), _vp]),
+    "sten_spmm_grouped_nm_batched": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(sten_spmm_problem),
+                                                    ctypes.c_int32, _vp]),
     "sten_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "sten_algo_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "sten_spmm_launch_count": (ctypes.c_int32, [ctypes.POINTER(sten_spmm_plan)]),
@@ -249,6 +257,24 @@ def spmm_grouped_nm_allgather(values: torch.Tensor, idx: torch.Tensor, B: torch.
         ptrs, len(outs), col0, ld, _dt(outs[0]), ctypes.byref(plan) if plan is not None else None,
         _stream(stream)), "sten_spmm_grouped_nm_allgather")
     return outs
+
+
+def spmm_grouped_nm_batched(problems, tile: int = 1, stream=None):
+    """ONE launch for several independent fp32 problems: problems = [(values, idx, B, n, m, g, C), ...];
+    each C [M][N] receives densify(values, idx) @ B (sten_spmm_grouped_nm_batched)."""
+    arr = (sten_spmm_problem * len(problems))()
+    for k, (values, idx, B, n, m, g, C) in enumerate(problems):
+        _cuda(B, "B")
+        arr[k].f = sten_nmg(n, m, g)
+        arr[k].values, arr[k].idx = values.data_ptr(), idx.data_ptr()
+        arr[k].M, arr[k].K = values.shape[0], B.shape[0]
+        arr[k].B, arr[k].ldb, arr[k].N = B.data_ptr(), _ld(B), B.shape[1]
+        arr[k].C, arr[k].ldc = C.data_ptr(), _ld(C)
+        if values.dtype != torch.float32 or B.dtype != torch.float32 or C.dtype != torch.float32:
+            raise TypeError("the grouped launch is fp32")
+    _check(load().sten_spmm_grouped_nm_batched(len(problems), arr, tile, _stream(stream)),
+           "sten_spmm_grouped_nm_batched")
+    return [p[6] for p in problems]
 
 
 ACT_NONE, ACT_GELU, ACT_RELU = 0, 1, 2

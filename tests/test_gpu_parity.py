@@ -496,3 +496,30 @@ def test_spmm_bias_act_epilogue(act, split, with_bias):
     # and erff (a few ulp of the result)
     tol = 1.13 * 1e-5 * Bound + 4e-7 * np.abs(Y) + 1e-7 * (np.abs(C_ref) + (np.abs(bias)[:, None] if with_bias else 0))
     assert (np.abs(C.cpu().numpy().astype(np.float64) - Y) <= tol + 1e-30).all()
+
+
+# ----------------------------------------------------------------------------------------
+# Grouped (batched) launch of independent problems
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("tile", [1, 2])
+def test_spmm_batched_equals_single_launches(tile):
+    """One grouped launch over mixed shapes / sparsities / ragged sizes equals the per-problem
+    launches (same tile, split_k = 1) bit for bit, and the oracle within 1e-5."""
+    g = 4
+    shapes = [(64, 96, 300, 2, 4), (120, 400, 129, 1, 10), (200, 64, 256, 1, 4), (56, 768, 40, 2, 4)]
+    probs, singles, refs = [], [], []
+    for k, (M, K, N, n, m) in enumerate(shapes):
+        W = synthetic.weights(M, K, seed=40 + k)
+        B = synthetic.activations(K, N, seed=50 + k)
+        v, i = gpu_sparsify(W, n, m, g, "f32")
+        Bd = dev(B, "f32")
+        C = torch.full((M, N), float("nan"), device="cuda")
+        probs.append((v, i, Bd, n, m, g, C))
+        singles.append(sten.spmm_grouped_nm(v, i, Bd, n, m, g, plan=sten.make_plan(sten.ALGO_SIMT, 1, tile)))
+        v_ref, i_ref = oracle.sparsify(W, n, m, g)
+        refs.append(oracle.spmm(v_ref, i_ref, B, n, m, g))
+    sten.spmm_grouped_nm_batched(probs, tile=tile)
+    torch.cuda.synchronize()
+    for (v, i, Bd, n, m, g_, C), S, (C_ref, Bound) in zip(probs, singles, refs):
+        assert torch.equal(C, S)
+        assert rel_err(C, C_ref, Bound) <= 1e-5
