@@ -640,7 +640,7 @@ def bench_e2e(cases, host, dtype, steps, device):
     # the cases are independent linears: spread over 3 streams (LPT on their copy bytes) so one
     # case's PCIe copies overlap another's kernels and H2D overlaps D2H; the step ends when the
     # main stream has joined every lane (all C_host written)
-    n_lanes = min(3, len(cases))
+    n_lanes = min(int(os.environ.get("STEN_E2E_LANES", "3")), len(cases))
     lanes = [torch.cuda.Stream(device) for _ in range(n_lanes)]
     lane_of = [0] * len(cases)
     load = [0.0] * n_lanes
