@@ -523,3 +523,29 @@ def test_spmm_batched_equals_single_launches(tile):
     for (v, i, Bd, n, m, g_, C), S, (C_ref, Bound) in zip(probs, singles, refs):
         assert torch.equal(C, S)
         assert rel_err(C, C_ref, Bound) <= 1e-5
+
+
+def test_new_entry_points_reject_bad_arguments():
+    """Argument errors of the fused / grouped entry points are returned before any launch."""
+    n, m, g, M, K, N = 2, 4, 4, 32, 64, 40
+    W = torch.from_numpy(synthetic.weights(M, K, seed=61)).cuda()
+    B = torch.from_numpy(synthetic.activations(K, N, seed=62)).cuda()
+    v, i = sten.sparsify_grouped_nm(W, n, m, g)
+    C = torch.zeros((M, N), device="cuda")
+    with pytest.raises(sten.StenError) as e:                                 # act out of range
+        sten.spmm_grouped_nm_bias_act(v, i, B, n, m, g, act=7, out=C)
+    assert e.value.status == 1
+    with pytest.raises(sten.StenError) as e:                                 # fused epilogue is SIMT-only
+        sten.spmm_grouped_nm_bias_act(v, i, B, n, m, g, act=1, out=C, plan=sten.make_plan(sten.ALGO_MMA_SYNC, 1, 1))
+    assert e.value.status == 3
+    with pytest.raises(sten.StenError) as e:                                 # gathered buffer too narrow
+        sten.spmm_grouped_nm_allgather(v, i, B, n, m, g, [torch.zeros((M, N), device="cuda")], 8)
+    assert e.value.status == 2
+    with pytest.raises(sten.StenError) as e:                                 # mixed row-group classes
+        v8, i8 = sten.sparsify_grouped_nm(W, n, m, 8)
+        sten.spmm_grouped_nm_batched([(v, i, B, n, m, 4, C), (v8, i8, B, n, m, 8, torch.zeros_like(C))])
+    assert e.value.status == 3
+    with pytest.raises(sten.StenError) as e:                                 # unknown tile
+        sten.spmm_grouped_nm_batched([(v, i, B, n, m, g, C)], tile=5)
+    assert e.value.status == 3
+    assert torch.count_nonzero(C) == 0                                       # nothing was written
