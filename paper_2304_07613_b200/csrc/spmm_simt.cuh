@@ -520,10 +520,11 @@ __device__ __forceinline__ void spmm_simt_body(const SpmmArgs& a, const CUtensor
                                 for (int j = 0; j < Cfg::kChunks; ++j) {
                                     float b[EV];
                                     unpack<EV>(lds128_addr(offs[t] + uint32_t(j) * 512u), b);
+                                    // b pair outer, rows inner: consecutive FFMA2 share the B operand
 #pragma unroll
-                                    for (int r = 0; r < RG; ++r)
+                                    for (int e = 0; e < EV; e += 2)
 #pragma unroll
-                                        for (int e = 0; e < EV; e += 2) {
+                                        for (int r = 0; r < RG; ++r) {
                                             float2& c2 = *reinterpret_cast<float2*>(&acc[q][r][j * EV + e]);
                                             c2 = __ffma2_rn(make_float2(v[r][t], v[r][t]), make_float2(b[e], b[e + 1]), c2);
                                         }
