@@ -238,6 +238,9 @@ __global__ void __launch_bounds__(256)
 sparsify_grouped_nm_kernel(const T* __restrict__ W, int64_t ldw, int64_t G, int64_t KB, int n,
                            int g, T* __restrict__ values, int64_t Kp, uint8_t* __restrict__ idx,
                            int aligned) {
+    // let a programmatically dependent SpMM launch now: its prologue overlaps this grid, its
+    // reads of values / idx wait (griddepcontrol.wait) until this grid has completed
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (tid >= G * KB) return;
     int64_t grp, kb;

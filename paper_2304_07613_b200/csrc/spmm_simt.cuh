@@ -369,6 +369,9 @@ __device__ __forceinline__ void spmm_simt_body(const SpmmArgs& a, const CUtensor
 
     if (warp == CW) {
         // ======================= producer warp =======================
+        // programmatic dependent launch: the prologue above overlapped the tail of the kernel
+        // that produced values / idx (the sparsifier); wait for it before the first read
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
         const TAB* __restrict__ V = static_cast<const TAB*>(a.values);
         const uint32_t v_bytes = a.v_tma ? uint32_t(BM * ksp * sizeof(TAB)) : 0u;
         const uint32_t tx_bytes = uint32_t(L.bk) * ROWB + v_bytes;

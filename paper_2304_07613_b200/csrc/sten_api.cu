@@ -210,13 +210,20 @@ sten_status launch_simt_cfg(SpmmArgs a, cudaStream_t st) {
     cfg.blockDim = dim3(Cfg::kThreads);                        // consumers + the producer warp
     cfg.dynamicSmemBytes = L.total;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = unsigned(a.split);
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL: overlap the prologue with
+    attr[na].val.programmaticStreamSerializationAllowed = 1;            // the previous kernel (sparsify)
+    ++na;
+    if (a.split > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 1;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = unsigned(a.split);
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = a.split > 1 ? 1 : 0;
+    cfg.numAttrs = na;
     if (cudaLaunchKernelEx(&cfg, kern, a, tmB, tmV) != cudaSuccess) return STEN_ERR_CUDA;
     return last_cuda();
 }
