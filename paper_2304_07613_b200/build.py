@@ -17,7 +17,7 @@ LIB = os.path.join(PKG, "libsten.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "--split-compile=0",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 
 
