@@ -132,8 +132,14 @@ nmg_sparsify_kernel(const NmgArgs a) {
     if (NI <= 32 * KPL) {
         // keys in registers; a key is zeroed when its column is taken or its pattern is full
         unsigned long long kr[KPL];
+        int kcol[KPL], kpat[KPL];                // each key's column and pattern, decoded once
 #pragma unroll
-        for (int j = 0; j < KPL; ++j) kr[j] = lane + 32 * j < NI ? make_key(lane + 32 * j) : 0ull;
+        for (int j = 0; j < KPL; ++j) {
+            const int i = lane + 32 * j;
+            kr[j] = i < NI ? make_key(i) : 0ull;
+            kcol[j] = i < NI ? i / C : -1;
+            kpat[j] = i < NI ? i - (i / C) * C : -1;
+        }
         for (int step = 0; step < L; ++step) {
             unsigned long long best = 0ull;
 #pragma unroll
@@ -147,7 +153,7 @@ nmg_sparsify_kernel(const NmgArgs a) {
             const bool full = c_old + 1 >= g;
 #pragma unroll
             for (int j = 0; j < KPL; ++j)
-                if (kr[j] != 0ull && (kb(kr[j]) == b || (full && kp(kr[j]) == p))) kr[j] = 0ull;
+                kr[j] = (kcol[j] == b || (full && kpat[j] == p)) ? 0ull : kr[j];
         }
     } else {
         for (int i = lane; i < NI; i += 32) key[i] = make_key(i);
