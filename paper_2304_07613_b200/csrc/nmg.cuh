@@ -87,6 +87,11 @@ template <typename T, int KPL>
 __global__ void __launch_bounds__(kNmgWarpsPerCta * 32)
 nmg_sparsify_kernel(const NmgArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    // kept row t of pattern p, tabulated once per CTA (the bit scan is not in the per-key path)
+    __shared__ int8_t spos[kNmgMaxPatterns * 16];
+    for (int e = threadIdx.x; e < a.C * a.n; e += blockDim.x)
+        spos[e] = int8_t(nmg_pos(a.pat.mask[e / a.n], e % a.n));
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t chunk = int64_t(blockIdx.x) * kNmgWarpsPerCta + warp;
     if (chunk >= a.RB * a.NC) return;
@@ -112,9 +117,8 @@ nmg_sparsify_kernel(const NmgArgs a) {
     const int NI = L * C;
     auto make_key = [&](int i) -> unsigned long long {
         const int b = i / C, p = i - b * C;
-        const uint32_t mk = a.pat.mask[p];
         float s = 0.0f;
-        for (int t = 0; t < n; ++t) s = __fadd_rn(s, fabsf(to_f32(sw[nmg_pos(mk, t) * L + b])));
+        for (int t = 0; t < n; ++t) s = __fadd_rn(s, fabsf(to_f32(sw[spos[p * n + t] * L + b])));
         return (static_cast<unsigned long long>(__float_as_uint(s)) << 32) |
                (static_cast<unsigned long long>(0xFFFFu - uint32_t(b)) << 16) | (0xFFFFu - uint32_t(p));
     };
@@ -179,8 +183,7 @@ nmg_sparsify_kernel(const NmgArgs a) {
         for (int b2 = 0; b2 < b; ++b2) rank += pat_of[b2] == p;
         const int64_t slot = base + int64_t(p) * g + rank;
         a.idx[slot] = uint16_t(b);
-        const uint32_t mk = a.pat.mask[p];
-        for (int t = 0; t < n; ++t) V[slot * n + t] = sw[nmg_pos(mk, t) * L + b];
+        for (int t = 0; t < n; ++t) V[slot * n + t] = sw[spos[p * n + t] * L + b];
     }
 }
 
