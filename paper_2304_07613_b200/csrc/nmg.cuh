@@ -133,7 +133,71 @@ nmg_sparsify_kernel(const NmgArgs a) {
     auto kb = [](unsigned long long k) { return int(0xFFFFu - uint32_t((k >> 16) & 0xFFFFu)); };
     auto kp = [](unsigned long long k) { return int(0xFFFFu - uint32_t(k & 0xFFFFu)); };
 
-    if (NI <= 32 * KPL) {
+    if (L <= 32 && C <= 8 && NI > 96) {      // (small chunks: the L-step loop below is cheaper)
+        // Round-based exact greedy (L <= 32: lane b owns column b).  The largest acceptable item
+        // is always the largest "proposal" (each free column's best not-full pattern), so in a
+        // round the warp sorts the proposals (bitonic, descending) and accepts the longest prefix
+        // in which no pattern exceeds its capacity g; a proposal to a pattern that fills inside
+        // the round ends it.  Identical to the sequential greedy, <= C + 1 rounds instead of L.
+        unsigned long long kc[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) kc[p] = (lane < L && p < C) ? make_key(lane * C + p) : 0ull;
+        int cntr[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) cntr[p] = 0;
+        bool assigned = lane >= L;
+        int mypat = -1;
+        __shared__ uint32_t acc_scratch[kNmgWarpsPerCta][32];      // per-warp column -> accepted pattern + 1
+        uint32_t* accf = acc_scratch[warp];
+        accf[lane] = 0u;
+        __syncwarp();
+        for (int round = 0; round <= C; ++round) {
+            unsigned long long prop = 0ull;
+            if (!assigned) {
+#pragma unroll
+                for (int p = 0; p < 8; ++p)
+                    if (p < C && cntr[p] < g && kc[p] > prop) prop = kc[p];
+            }
+            if (!__any_sync(0xffffffffu, prop != 0ull)) break;
+            // bitonic sort of the 32 proposals, descending across lanes
+            unsigned long long v = prop;
+#pragma unroll
+            for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, j);
+                    const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+                    const unsigned long long mn = o < v ? o : v, mx = o < v ? v : o;
+                    v = (lower == up) ? mx : mn;
+                }
+            // sorted position `lane` holds v; its pattern, and how many earlier positions share it
+            const bool real = v != 0ull;
+            const int vp = real ? kp(v) : -1;
+            const unsigned same = __match_any_sync(0xffffffffu, vp);
+            const int before = __popc(same & ((1u << lane) - 1u));            // earlier, same pattern
+            int cp = 0;
+#pragma unroll
+            for (int p = 0; p < 8; ++p) cp = (p == vp) ? cntr[p] : cp;
+            const bool ok = real && cp + before + 1 <= g;
+            const unsigned bad = __ballot_sync(0xffffffffu, real && !ok);
+            const int stop = bad ? __ffs(bad) - 1 : 32;
+            const bool acc = real && lane < stop;
+            // tell each column lane whether its proposal was accepted (inverse permutation via smem)
+            if (acc) accf[kb(v)] = uint32_t(vp) + 1u;
+            __syncwarp();
+            if (!assigned && lane < L) {
+                const uint32_t f = accf[lane];
+                if (f) { assigned = true; mypat = int(f) - 1; }
+            }
+            __syncwarp();
+            if (acc) accf[kb(v)] = 0u;
+            // capacity update, identical in every lane
+#pragma unroll
+            for (int p = 0; p < 8; ++p) cntr[p] += __popc(__ballot_sync(0xffffffffu, acc && vp == p));
+            __syncwarp();
+        }
+        if (lane < L) pat_of[lane] = int16_t(mypat);
+    } else if (NI <= 32 * KPL) {
         // keys in registers; a key is zeroed when its column is taken or its pattern is full
         unsigned long long kr[KPL];
         int kcol[KPL], kpat[KPL];                // each key's column and pattern, decoded once
