@@ -94,8 +94,16 @@ def eff_flops(c) -> float:          # dense-equivalent, true (unpadded) K
     return 2.0 * c.M * c.K * c.N
 
 
-def nz_flops(c) -> float:           # algorithmic MACs actually required (kept K', incl. K padding)
-    return 2.0 * c.M * c.kept * c.N
+def kept_min(c) -> int:
+    """Kept entries per row of the method itself: ceil(K/m) n (one zero-padded block at most,
+    DESIGN.md R7).  The extra zero columns the bench appends for 16-byte aligned values rows
+    (1:10: K 768 -> 800, K' 80 instead of 77) are padding, not the method's work, and are not
+    counted in the roofline's algorithmic flops or bytes."""
+    return -(-c.K // c.m) * c.n
+
+
+def nz_flops(c) -> float:           # algorithmic flops: 2 M K' N with the method's K'
+    return 2.0 * c.M * kept_min(c) * c.N
 
 
 def esize(dtype):
@@ -105,13 +113,15 @@ def esize(dtype):
 def spmm_bytes(c, out_size=None) -> float:
     s = esize(c.dtype)
     so = s if out_size is None else out_size
-    return c.M * c.kept * s + (c.M // c.g) * (c.Kp // c.m) * c.n + c.Kp * c.N * s + c.M * c.N * so
+    kb = -(-c.K // c.m)
+    return c.M * kept_min(c) * s + (c.M // c.g) * kb * c.n + kb * c.m * c.N * s + c.M * c.N * so
 
 
 def sparsify_bytes(c) -> float:
     """HBM roofline bytes of one sparsify launch: read W, write values and idx."""
     s = esize(c.dtype)
-    return c.M * c.Kp * s + c.M * c.kept * s + (c.M // c.g) * (c.Kp // c.m) * c.n
+    kb = -(-c.K // c.m)
+    return c.M * kb * c.m * s + c.M * kept_min(c) * s + (c.M // c.g) * kb * c.n
 
 
 def cores() -> int:
@@ -511,7 +521,9 @@ def bench_sten(args, rank, world, local_rank):
         out["clocks"] = clocks
     if not args.profile:
         out["context_dense"] = dense_context(cases, sets[0], dtype, device)
-    return out, cases, host, dtype, g
+    # the timed step's results (every set holds the same inputs) for bench's own parity check
+    gpu_out = [(d["idx"].cpu().numpy(), d["C"].float().cpu().numpy()) for d in sets[0]]
+    return out, cases, host, dtype, g, gpu_out
 
 
 def per_kernel_b2b(cases, data, dtype, device, l2, steps):
@@ -692,9 +704,10 @@ def bench_e2e(cases, host, dtype, steps, device):
 # ------------------------------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline leg and --impl reference)
 # ------------------------------------------------------------------------------------------------
-def oracle_step_time(cases, host, sample_cols, nthreads):
+def oracle_step_time(cases, host, sample_cols, nthreads, keep=None):
     """Time the oracle on one step: sparsify every full W, SpMM on `sample_cols` columns.
-    Returns (seconds extrapolated to the full step, seconds spent, sparsify s, spmm s per column)."""
+    Returns (seconds extrapolated to the full step, seconds spent, sparsify s, spmm s per column).
+    keep: a list that receives (idx, C[:, :sample_cols], Bound) per case (the parity check)."""
     import oracle
     t_sp = t_mm_col = t_full = t_spent = 0.0
     for c, (W, B) in zip(cases, host):
@@ -703,13 +716,33 @@ def oracle_step_time(cases, host, sample_cols, nthreads):
         t1 = time.perf_counter()
         ns = min(sample_cols, c.N)
         Bs = np.ascontiguousarray(B[:, :ns])
-        oracle.spmm(v, i, Bs, c.n, c.m, c.g, nthreads=nthreads, with_bound=False)
+        C = oracle.spmm(v, i, Bs, c.n, c.m, c.g, nthreads=nthreads, with_bound=False)
         t2 = time.perf_counter()
         t_sp += t1 - t0
         t_mm_col += (t2 - t1) / ns
         t_full += (t1 - t0) + (t2 - t1) * (c.N / ns)
         t_spent += t2 - t0
+        if keep is not None:
+            # the error bound sum |v| |b| of the sampled columns (fp64), outside the timed work
+            C, Bound = oracle.spmm(v, i, Bs, c.n, c.m, c.g, nthreads=nthreads, with_bound=True)
+            keep.append((i, C, Bound, ns))
     return t_full, t_spent, t_sp, t_mm_col
+
+
+def parity_check(cases, gpu_out, oracle_out):
+    """bench.py's own check of its timed outputs: idx bit-exact on the whole weight, C on the
+    oracle's sampled columns within the north_star tolerance (rel = |C - C_ref| / sum |v||b|;
+    1e-5 fp32, 2e-2 bf16).  gpu_out = [(idx, C)] host copies of the timed step's results."""
+    worst = 0.0
+    for c, (gi, gC), (oi, oC, Bound, ns) in zip(cases, gpu_out, oracle_out):
+        if not np.array_equal(gi, oi):
+            return False, "idx mismatch in %s" % c.label(), worst
+        Cg = gC[:, :ns].astype(np.float64)
+        err = float(np.max(np.abs(Cg - oC) / np.maximum(Bound, 1e-30))) if Cg.size else 0.0
+        worst = max(worst, err)
+        if err > (1e-5 if c.dtype == "f32" else 2e-2):
+            return False, "C rel err %.3g in %s" % (err, c.label()), worst
+    return True, "ok", worst
 
 
 def calibrate_cols(cases, host, nthreads, budget_s):
@@ -719,7 +752,7 @@ def calibrate_cols(cases, host, nthreads, budget_s):
     return max(8, min(cases[0].N, cols // 8 * 8))
 
 
-def cpu_baseline(cases, host, budget_s=15.0):
+def cpu_baseline(cases, host, budget_s=15.0, keep=None):
     import oracle
     oracle.build()
     nt = cores()
@@ -732,6 +765,8 @@ def cpu_baseline(cases, host, budget_s=15.0):
         spent += t_spent
         if spent >= budget_s or len(fulls) >= 50:
             break
+    if keep is not None:                     # the oracle results of the same sample, untimed
+        oracle_step_time(cases, host, cols, nt, keep=keep)
     t_full = statistics.median(fulls)
     val = sum(eff_flops(c) for c in cases) / t_full / 1e9
     return {"value": round(val, 4), "unit": UNIT, "cores": nt, "kind": "oracle",
@@ -801,7 +836,7 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    out, cases, host, dtype, g = bench_sten(args, rank, world, local_rank)
+    out, cases, host, dtype, g, gpu_out = bench_sten(args, rank, world, local_rank)
     if not args.profile:
         if not args.no_e2e:
             e2e = bench_e2e(cases, host, dtype, max(3, min(args.steps, 10)), torch.device("cuda", local_rank))
@@ -811,7 +846,17 @@ def main():
                 e2e["value"] = round(float(t.item()) * world, 2)
             out["e2e"] = e2e
         if rank == 0 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(cases, host)
+            keep = []
+            out["cpu_baseline"] = cpu_baseline(cases, host, keep=keep)
+            ok, why, worst = parity_check(cases, gpu_out, keep)
+            out["parity_checked"] = ok
+            out["parity"] = {"what": "timed step's idx (whole weight, bit-exact) and C on the cpu_baseline's %d "
+                                     "sampled token columns per case vs the oracle" % keep[0][3],
+                             "max_rel_err": worst, "status": why}
+            if not ok:
+                print(json.dumps(out), flush=True)
+                print("PARITY FAILURE: " + why, file=sys.stderr, flush=True)
+                return 3
     if world > 1:
         dist.barrier()
     if rank == 0:

@@ -117,7 +117,7 @@ class TokenShardedSpmm:
             if hi > c0:
                 self.compute(B_local[:, c0:hi], piece[:, : hi - c0])
             gathered = torch.empty((world * M, c1 - c0), dtype=self.out_dtype, device=self.device)
-            if self.use_streams:
+            if self.use_streams and world > 1:
                 ev = torch.cuda.Event()
                 ev.record(compute_stream)
                 with torch.cuda.stream(self.comm_stream):
@@ -131,14 +131,14 @@ class TokenShardedSpmm:
             else:
                 gathered.copy_(piece)
             staged.append(gathered)
-        if self.use_streams:
+        if self.use_streams and world > 1:
             compute_stream.wait_stream(self.comm_stream)
-        # assemble: rank p's local column j is global column p * n_local + j
-        full = torch.empty((M, world * nl), dtype=self.out_dtype, device=self.device)
+        # assemble: rank p's local column j is global column p * n_local + j -- one strided copy
+        # per chunk ([world][M][cw] gathered block -> columns {p n_local + c0 ..} of every rank p)
+        full = torch.empty((M, world, nl), dtype=self.out_dtype, device=self.device)
         for (c0, c1), gathered in zip(bounds, staged):
-            for p in range(world):
-                full[:, p * nl + c0: p * nl + c1] = gathered[p * M:(p + 1) * M]
-        return full[:, : self.N_global]
+            full[:, :, c0:c1].copy_(gathered.view(world, M, c1 - c0).permute(1, 0, 2))
+        return full.view(M, world * nl)[:, : self.N_global]
 
 
 class RowShardedSpmm:
@@ -194,19 +194,30 @@ class FusedAllGatherSpmm:
         self.world, self.rank = _world(self.group)
         self.N_global = N_global
         self.n_local = padded_shard_width(N_global, self.world)
-        # the GLOBAL plan (pin P11), restricted to the fused-epilogue kernel (SIMT)
+        # the GLOBAL plan (pin P11), restricted to the fused-epilogue kernel (SIMT).  When the automatic
+        # choice for the global shape is another algorithm its tile / split numbers mean something else,
+        # so a concrete SIMT plan is used instead (tile 1 exists for fp32 and bf16; one K partition) --
+        # identical on every rank and independent of the local width.
         plan = sten.spmm_plan(n, m, g, self.M, K, N_global, ab_dtype=values.dtype, c_dtype=self.out_dtype)
-        plan.algo = sten.ALGO_SIMT if plan.algo != sten.ALGO_SIMT else plan.algo
+        if plan.algo != sten.ALGO_SIMT:
+            plan = sten.make_plan(sten.ALGO_SIMT, split_k=1, tile=1)
         self.plan = plan
         ldc = self.world * self.n_local
         self.buf = symm_mem.empty((self.M, ldc), dtype=self.out_dtype, device=values.device)
         self.handle = symm_mem.rendezvous(self.buf, self.group)
         self.peers = [self.handle.get_buffer(p, (self.M, ldc), self.out_dtype) for p in range(self.world)]
 
-    def forward(self, B_local: torch.Tensor) -> torch.Tensor:
-        """C [M][N_global] on every rank; B_local = this rank's columns of B."""
+    def forward(self, B_local: torch.Tensor, copy: bool = False) -> torch.Tensor:
+        """C [M][N_global] on every rank; B_local = this rank's columns of B.
+
+        The result is a view of the persistent symmetric buffer: it stays valid until the next
+        forward() (which overwrites it on every rank); pass copy=True for an independent tensor."""
         from . import sten
+        # pre-barrier: no rank may start storing into its peers' buffers while a peer's stream is
+        # still reading the previous step's result (write-after-read across ranks)
+        self.handle.barrier(channel=0)
         sten.spmm_grouped_nm_allgather(self.values, self.idx, B_local, self.n, self.m, self.g, self.peers,
                                        self.rank * self.n_local, plan=self.plan)
         self.handle.barrier(channel=0)          # every peer's stores into this buffer have landed
-        return self.buf[:, : self.N_global]
+        out = self.buf[:, : self.N_global]
+        return out.clone() if copy else out

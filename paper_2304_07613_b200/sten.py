@@ -132,6 +132,23 @@ def _cuda(t: torch.Tensor, name: str):
         raise ValueError("%s must be 2-D" % name)
 
 
+def _check_operands(values: torch.Tensor, idx: torch.Tensor, B: torch.Tensor):
+    """The C ABI assumes packed values [M][K'] / idx [M/g][K/m][n] on the current device and one
+    A/B element type: reject anything else instead of letting the kernel reinterpret bytes."""
+    _cuda(values, "values")
+    _cuda(B, "B")
+    if values.dtype != B.dtype:
+        raise TypeError("values (%s) and B (%s) must share a dtype" % (values.dtype, B.dtype))
+    if idx.dtype != torch.uint8:
+        raise TypeError("idx must be uint8")
+    if not values.is_contiguous() or not idx.is_contiguous():
+        raise ValueError("values and idx must be contiguous (packed [M][K'] / [M/g][K/m][n])")
+    dev = torch.cuda.current_device()
+    for t, nm in ((values, "values"), (idx, "idx"), (B, "B")):
+        if t.device.index != dev:
+            raise ValueError("%s is on cuda:%s, the current device is cuda:%d" % (nm, t.device.index, dev))
+
+
 def _ld(t: torch.Tensor) -> int:
     if t.stride(-1) != 1:
         raise ValueError("innermost dimension must be contiguous")
@@ -208,12 +225,9 @@ def spmm_grouped_nm(values: torch.Tensor, idx: torch.Tensor, B: torch.Tensor, n:
                     out: torch.Tensor | None = None, out_dtype=None, plan: sten_spmm_plan | None = None,
                     stream=None) -> torch.Tensor:
     """a5-a7: C [M][N] = densify(values, idx) @ B  (B [K][N])."""
-    _cuda(values, "values")
-    _cuda(B, "B")
+    _check_operands(values, idx, B)
     M = values.shape[0]
     K, N = B.shape
-    if values.dtype != B.dtype:
-        raise TypeError("values and B must share a dtype")
     if out is None:
         out = torch.empty((M, N), dtype=out_dtype or B.dtype, device=B.device)
     lib = load()
@@ -229,8 +243,7 @@ def spmm_grouped_nm(values: torch.Tensor, idx: torch.Tensor, B: torch.Tensor, n:
 def spmm_autotune(values: torch.Tensor, idx: torch.Tensor, B: torch.Tensor, n: int, m: int, g: int,
                   out: torch.Tensor, reps: int = 5, stream=None) -> sten_spmm_plan:
     """Fastest compiled plan for this shape, measured on the device (out is scratch)."""
-    _cuda(values, "values")
-    _cuda(B, "B")
+    _check_operands(values, idx, B)
     M = values.shape[0]
     K, N = B.shape
     plan = sten_spmm_plan()
@@ -245,7 +258,7 @@ def spmm_grouped_nm_allgather(values: torch.Tensor, idx: torch.Tensor, B: torch.
     """C_loc = densify(values, idx) @ B written by the SpMM epilogue into columns [col0, col0 + N) of
     EVERY buffer in `outs` (the gathered [M][ldc] outputs of all ranks: peer-mapped views, or
     local tensors) -- sten_spmm_grouped_nm_allgather."""
-    _cuda(B, "B")
+    _check_operands(values, idx, B)
     M = values.shape[0]
     K, N = B.shape
     ld = _ld(outs[0])
@@ -264,7 +277,7 @@ def spmm_grouped_nm_batched(problems, tile: int = 1, stream=None):
     each C [M][N] receives densify(values, idx) @ B (sten_spmm_grouped_nm_batched)."""
     arr = (sten_spmm_problem * len(problems))()
     for k, (values, idx, B, n, m, g, C) in enumerate(problems):
-        _cuda(B, "B")
+        _check_operands(values, idx, B)
         arr[k].f = sten_nmg(n, m, g)
         arr[k].values, arr[k].idx = values.data_ptr(), idx.data_ptr()
         arr[k].M, arr[k].K = values.shape[0], B.shape[0]
@@ -284,7 +297,7 @@ def spmm_grouped_nm_bias_act(values: torch.Tensor, idx: torch.Tensor, B: torch.T
                              bias: torch.Tensor | None = None, act: int = ACT_GELU, out: torch.Tensor | None = None,
                              out_dtype=None, plan: sten_spmm_plan | None = None, stream=None) -> torch.Tensor:
     """C = act(densify(values, idx) @ B + bias[:, None]) with the bias/activation in the SpMM epilogue."""
-    _cuda(B, "B")
+    _check_operands(values, idx, B)
     M = values.shape[0]
     K, N = B.shape
     if out is None:

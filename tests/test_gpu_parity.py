@@ -293,17 +293,35 @@ def test_host_e2e_entry_point():
 # ----------------------------------------------------------------------------------------
 # BASELINE.json sizes, in the launch configuration bench.py uses: sampled outputs
 # ----------------------------------------------------------------------------------------
+def _plan_cache(cfg, dtype, g):
+    import json, os
+    path = os.path.join(os.path.dirname(sten.__file__), "plans", "c%d_%s_g%d_step.json" % (cfg + 1, dtype, g))
+    if not os.path.exists(path):
+        return {}
+    with open(path) as f:
+        return json.load(f)
+
+
 @pytest.mark.parametrize("cfg", [1, 2])
 def test_baseline_configs_sampled(cfg):
+    """Every case of C2 (all 9) and C3 at full size, with the plans bench.py times (the step-tuned
+    plan cache where it has the case, else AUTO): sparsify bit-exact on the whole weight, the
+    product on sampled token columns against the oracle."""
     rng = np.random.default_rng(cfg)
-    cases = synthetic.config_cases(cfg, g=4 if cfg == 1 else 16)
-    for case in cases[:: 3 if cfg == 1 else 1]:
-        W = synthetic.weights(case.M, case.K, seed=1234 + cfg, dtype=case.dtype, k_pad=case.k_pad)
-        B = synthetic.activations(case.K, case.N, seed=1234 + cfg, dtype=case.dtype, k_pad=case.k_pad)
+    g = 4 if cfg == 1 else 16
+    cases = synthetic.config_cases(cfg, g=g)
+    cache = _plan_cache(cfg, cases[0].dtype, g)
+    for ci, case in enumerate(cases):
+        W = synthetic.weights(case.M, case.K, seed=1234 + ci, dtype=case.dtype, k_pad=case.k_pad)
+        B = synthetic.activations(case.K, case.N, seed=1234 + ci, dtype=case.dtype, k_pad=case.k_pad)
         v_ref, i_ref = oracle.sparsify(W, case.n, case.m, case.g)
         v, i = gpu_sparsify(W, case.n, case.m, case.g, case.dtype)
         assert np.array_equal(host(i), i_ref)
-        C = sten.spmm_grouped_nm(v, i, dev(B, case.dtype), case.n, case.m, case.g, out_dtype=torch.float32)
+        assert np.array_equal(host(v).view(np.uint8), v_ref.view(np.uint8))
+        pd = cache.get(case.label())
+        plan = sten.make_plan(pd["algo"], pd["split_k"], pd["tile"]) if pd else None
+        C = sten.spmm_grouped_nm(v, i, dev(B, case.dtype), case.n, case.m, case.g, out_dtype=torch.float32,
+                                 plan=plan)
         cols = np.sort(rng.choice(case.N, size=24, replace=False))
         Cs = C.cpu().numpy()[:, cols].astype(np.float64)
         C_ref, Bound = oracle.spmm(v_ref, i_ref, np.ascontiguousarray(B[:, cols]), case.n, case.m, case.g,
@@ -455,22 +473,28 @@ def test_spmm_fused_allgather_equals_unsharded(split, P):
     torch.cuda.synchronize()
     for o in outs:
         assert torch.equal(o, C_full)
+    v_ref, i_ref = oracle.sparsify(W, n, m, g)
+    C_ref, Bound = oracle.spmm(v_ref, i_ref, B, n, m, g)
+    assert rel_err(outs[0], C_ref, Bound) <= 1e-5
     with pytest.raises(sten.StenError):                   # the fused epilogue is the SIMT kernel's
         sten.spmm_grouped_nm_allgather(v, i, Bd[:, :per], n, m, g, outs, 0,
                                        plan=sten.make_plan(sten.ALGO_MMA_SYNC, 1, 1))
 
 
-def test_fused_allgather_symmetric_memory_world1():
-    """parallel.FusedAllGatherSpmm end to end on a one-rank NCCL group: symmetric-memory
-    rendezvous, peer views, the fused-epilogue SpMM and the device barrier (the 8-GPU case runs
-    the same code with 8 peer views)."""
+def test_partitions_nccl_world1_vs_oracle():
+    """Every partition class of parallel.py (TokenShardedSpmm with the chunked NCCL all-gather on
+    its side stream, RowShardedSpmm, FusedAllGatherSpmm on symmetric memory) on a one-rank NCCL
+    group with the real CUDA compute, compared element by element with the oracle (fp32 1e-5,
+    bf16 2e-2) and bit for bit with the unsharded product under the global plan (P11); fp32 and
+    bf16 (g = 64 forces the fused path's SIMT plan coercion)."""
     import os, socket, subprocess, sys
     s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    out = subprocess.run([sys.executable, os.path.join(root, "tools", "fused_allgather_w1.py")], cwd=root, env=env,
-                         capture_output=True, text=True, timeout=300)
-    assert "fused world=1 equal: True" in out.stdout, out.stdout + out.stderr
+    out = subprocess.run([sys.executable, os.path.join(root, "tests", "_dist_world1.py")], cwd=root, env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert "ALL OK" in out.stdout, out.stdout + out.stderr
+    assert out.stdout.count("CASE ") == 4 * 6
 
 
 # ----------------------------------------------------------------------------------------
