@@ -53,6 +53,22 @@ def group_range(M: int, g: int, world: int, rank: int) -> tuple[int, int]:
     return (rank * G // world) * g, ((rank + 1) * G // world) * g
 
 
+def aligned_rows(B: torch.Tensor) -> torch.Tensor:
+    """B itself when its rows start on 16-byte boundaries (the TMA contract of the C ABI:
+    16-byte aligned base and row pitch), else a copy into a buffer whose pitch is rounded up
+    to 16 bytes -- a layout copy (device-memory plumbing), no arithmetic."""
+    es = B.element_size()
+    if B.dim() != 2 or B.shape[1] == 0 or B.device.type != "cuda":
+        return B
+    if B.stride(1) == 1 and (B.stride(0) * es) % 16 == 0 and B.data_ptr() % 16 == 0:
+        return B
+    pitch = -(-B.shape[1] * es // 16) * 16 // es
+    buf = torch.empty((B.shape[0], pitch), dtype=B.dtype, device=B.device)
+    out = buf[:, : B.shape[1]]
+    out.copy_(B)
+    return out
+
+
 def _world(group):
     if dist.is_available() and dist.is_initialized():
         return dist.get_world_size(group), dist.get_rank(group)
@@ -107,6 +123,7 @@ class TokenShardedSpmm:
         """Compute the local shard chunk by chunk and all-gather every chunk as soon as it
         is done (side stream on GPUs).  Returns C [M][N_global]."""
         M, nl, world = self.M, self.n_local, self.world
+        B_local = aligned_rows(B_local)
         have = B_local.shape[1]
         bounds = self._chunk_bounds()
         staged = []
@@ -158,6 +175,7 @@ class RowShardedSpmm:
         maxr = max(r1 - r0 for r0, r1 in rows)
         local = torch.zeros((maxr, self.N), dtype=self.out_dtype, device=self.device)
         nr = self.r1 - self.r0
+        B = aligned_rows(B)
         if nr:
             self.compute(B, local[:nr])
         gathered = torch.empty((self.world * maxr, self.N), dtype=self.out_dtype, device=self.device)
@@ -215,6 +233,7 @@ class FusedAllGatherSpmm:
         from . import sten
         # pre-barrier: no rank may start storing into its peers' buffers while a peer's stream is
         # still reading the previous step's result (write-after-read across ranks)
+        B_local = aligned_rows(B_local)
         self.handle.barrier(channel=0)
         sten.spmm_grouped_nm_allgather(self.values, self.idx, B_local, self.n, self.m, self.g, self.peers,
                                        self.rank * self.n_local, plan=self.plan)

@@ -45,7 +45,7 @@ def main():
         Bt = torch.from_numpy(B.view(np.int16) if dtype == "bf16" else B)
         if dtype == "bf16":
             Wt, Bt = Wt.view(torch.bfloat16), Bt.view(torch.bfloat16)
-        Wd, Bd = Wt.cuda(), Bt.cuda()
+        Wd, Bd = Wt.cuda(), parallel.aligned_rows(Bt.cuda())   # 16-byte row pitch (TMA contract)
         v, i = sten.sparsify_grouped_nm(Wd, n, m, g)
         v_ref, i_ref = oracle.sparsify(W, n, m, g)
         C_ref, Bound = oracle.spmm(v_ref, i_ref, B, n, m, g)
