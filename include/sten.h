@@ -275,6 +275,43 @@ sten_status sten_sparse_linear_host_async(sten_nmg f, sten_dtype ab_dt,
                                           void* C_host, int64_t ldc, sten_dtype c_dt,
                                           void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * K6: the 2:4 structured-sparse tensor-core path (NEXT-4; bf16 in, fp32 accumulate).
+ *
+ * Every grouped n:m mask with n == 1 (any m) or n == 2 and 4 | m is also a 2:4
+ * mask on the aligned 4-windows of K (a 4-window meets at most two m-blocks for
+ * n = 1 and lies inside one block when 4 | m), so C = densify(values, idx) x B
+ * runs on tcgen05.mma.sp with the weight as the compressed
+ * A operand.  The group structure is carried by idx; any g | M.
+ *
+ * Packed operand (caller-allocated, sizes from sten_sp24_packed_size):
+ *   v24  [M128][K128/2] bf16: per row, 2 stored values per 4-window of K in
+ *        ascending position (an explicit 0 where the window keeps < 2 entries);
+ *        M128 / K128 = M / K rounded up to 128, padding rows/windows are 0.
+ *   meta [M128/128][K128/128][128][4] uint32: the 2-bit in-window positions,
+ *        one 32-bit word per (128-row block, 32 logical k, TMEM lane) in the
+ *        tensor-memory lane layout of the sparse MMA:
+ *        row r, 4-window j of the 32 -> lane r%8 + 16(r/16) + 8(j/4),
+ *        nibble j%4 + 4((r/8)%2); nibble = pos0 | pos1 << 2, pos0 < pos1.
+ * Formats: n == 1, or n == 2 with m % 4 == 0 (else STEN_ERR_UNSUPPORTED).
+ * --------------------------------------------------------------------------- */
+sten_status sten_sp24_packed_size(sten_nmg f, int64_t M, int64_t K,
+                                  int64_t* v24_bytes, int64_t* meta_bytes);
+
+/* (values, idx) of sten_sparsify_grouped_nm (bf16) -> (v24, meta).  A layout
+ * conversion (bit copies of the kept values), HBM-bound; v24 / meta 4-byte aligned. */
+sten_status sten_sp24_pack(sten_nmg f, sten_dtype dt, const void* values, const uint8_t* idx,
+                           int64_t M, int64_t K, void* v24, uint32_t* meta, void* stream);
+
+/* C [M][ldc] (c_dt, overwritten) = densify(values, idx) x B, B [K][ldb] bf16
+ * (B base, v24 and meta 16-byte aligned, ldb % 8 == 0).  tile: 0 = default,
+ * 1 = 256 rows x 128 tokens (3 stages), 2 = 256 x 192, 3 = 384 x 128,
+ * 4 = 128 x 256, 5 = 128 x 128 (4 stages).  fp32 accumulation in TMEM over
+ * K in ascending 32-k steps (independent of N and the token tiling). */
+sten_status sten_spmm_sp24(const void* v24, const uint32_t* meta, int64_t M, int64_t K,
+                           const void* B, int64_t ldb, int64_t N,
+                           void* C, int64_t ldc, sten_dtype c_dt, int32_t tile, void* stream);
+
 const char* sten_status_string(sten_status s);
 const char* sten_algo_name(int32_t algo);
 /* Number of kernel launches the last call of each entry point enqueues is

@@ -83,6 +83,10 @@ SIGNATURES = {
                                                      ctypes.POINTER(sten_spmm_plan), _vp]),
     "sten_spmm_grouped_nm_batched": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(sten_spmm_problem),
                                                     ctypes.c_int32, _vp]),
+    "sten_sp24_packed_size": (ctypes.c_int, [sten_nmg, _i64, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "sten_sp24_pack": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "sten_spmm_sp24": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, ctypes.c_int,
+                                      ctypes.c_int32, _vp]),
     "sten_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "sten_algo_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "sten_spmm_launch_count": (ctypes.c_int32, [ctypes.POINTER(sten_spmm_plan)]),
@@ -399,4 +403,43 @@ def nmg_spmm(values: torch.Tensor, idx: torch.Tensor, B: torch.Tensor, n: int, m
     _check(load().sten_nmg_spmm(sten_nmg(n, m, g), _dt(values), values.data_ptr(), idx.data_ptr(), M, K,
                                 B.data_ptr(), _ld(B), N, out.data_ptr(), _ld(out), _dt(out), _stream(stream)),
            "sten_nmg_spmm")
+    return out
+
+
+# ---- K6: 2:4 structured-sparse tensor-core path (NEXT-4) --------------------------------------
+
+def sp24_compatible(n: int, m: int) -> bool:
+    """Grouped n:m formats whose every pattern is 2:4 on aligned 4-windows of K."""
+    return n == 1 or (n == 2 and m % 4 == 0)
+
+
+def sp24_pack(values: torch.Tensor, idx: torch.Tensor, n: int, m: int, g: int, K: int, stream=None):
+    """(values, idx) -> (v24 [M128][K128/2] bf16, meta uint32) for sten_spmm_sp24 (sten_sp24_pack)."""
+    _cuda(values, "values")
+    if values.dtype != torch.bfloat16 or idx.dtype != torch.uint8:
+        raise TypeError("sp24 packs bf16 values with uint8 idx")
+    M = values.shape[0]
+    vb, mb = _i64(), _i64()
+    lib = load()
+    _check(lib.sten_sp24_packed_size(sten_nmg(n, m, g), M, K, ctypes.byref(vb), ctypes.byref(mb)),
+           "sten_sp24_packed_size")
+    M128 = -(-M // 128) * 128
+    v24 = torch.empty((M128, vb.value // 2 // max(M128, 1)), dtype=torch.bfloat16, device=values.device)
+    meta = torch.empty((mb.value // 4,), dtype=torch.int32, device=values.device)
+    _check(lib.sten_sp24_pack(sten_nmg(n, m, g), BF16, values.data_ptr(), idx.data_ptr(), M, K, v24.data_ptr(),
+                              meta.data_ptr(), _stream(stream)), "sten_sp24_pack")
+    return v24, meta
+
+
+def spmm_sp24(v24: torch.Tensor, meta: torch.Tensor, M: int, K: int, B: torch.Tensor,
+              out: torch.Tensor | None = None, out_dtype=None, tile: int = 0, stream=None) -> torch.Tensor:
+    """C [M][N] = densify(values, idx) @ B on the 2:4 sparse tensor cores (sten_spmm_sp24)."""
+    _cuda(B, "B")
+    if B.dtype != torch.bfloat16:
+        raise TypeError("sten_spmm_sp24 takes bf16 B")
+    N = B.shape[1]
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype or torch.bfloat16, device=B.device)
+    _check(load().sten_spmm_sp24(v24.data_ptr(), meta.data_ptr(), M, K, B.data_ptr(), _ld(B), N, out.data_ptr(),
+                                 _ld(out), _dt(out), int(tile), _stream(stream)), "sten_spmm_sp24")
     return out
