@@ -74,6 +74,9 @@ def parse_args():
                    help="ignore the step-tuned plan cache (paper_2304_07613_b200/plans/) and autotune per case")
     p.add_argument("--lanes", type=int, default=9,
                    help="streams the independent cases of a step are spread over (inside the graph)")
+    p.add_argument("--step-mode", choices=["grouped", "streams"], default=None,
+                   help="grouped: the step's SpMMs as ONE grouped split-K launch (sten_spmm_grouped_nm_batched_ex, "
+                        "default for fp32); streams: one launch per case spread over --lanes streams")
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu legs)")
     p.add_argument("--out", default=None, help="also append the JSON line to this file")
     return p.parse_args()
@@ -245,11 +248,50 @@ def assign_lanes(cases, lanes: int):
     return lane_of
 
 
-def run_step(cases, data, ev_pairs=None, ext=None, stream=None, lane_streams=None, lane_of=None):
+def grouped_problems(cases, data):
+    return [(d["values"], d["idx"], d["B"], c.n, c.m, c.g, d["C"]) for c, d in zip(cases, data)]
+
+
+def run_step(cases, data, ev_pairs=None, ext=None, stream=None, lane_streams=None, lane_of=None, grouped=None):
     """One step: sparsify + SpMM of every case.  With lane streams, the cases (independent
-    linears) run on several streams forked from / joined to `stream`."""
+    linears) run on several streams forked from / joined to `stream`.  grouped = (tile, workspace):
+    the sparsifiers on the lanes, then ONE grouped split-K launch of all SpMMs on `stream`."""
     import torch
     from paper_2304_07613_b200 import sten
+    if grouped is not None:
+        # the step's weights in one grouped sparsify call (one launch per (m, n) class), then the
+        # grouped SpMM (programmatic dependent launch: its prologue overlaps the sparsifier's tail)
+        classes = sorted({(c.m, c.n) for c in cases})
+        if lane_streams and len(classes) > 1:
+            # one grouped sparsify call per (m, n) class, the classes on separate streams
+            fork = torch.cuda.Event()
+            fork.record(stream)
+            for j, cl in enumerate(classes):
+                ls = lane_streams[j % len(lane_streams)]
+                ls.wait_event(fork)
+                with torch.cuda.stream(ls):
+                    sten.sparsify_grouped_nm_batched([(d["W"], c.n, c.m, c.g, d["values"], d["idx"])
+                                                      for c, d in zip(cases, data) if (c.m, c.n) == cl])
+            for ls in lane_streams[:len(classes)]:
+                stream.wait_stream(ls)
+        else:
+            with torch.cuda.stream(stream):
+                if ev_pairs is not None:
+                    for k in range(len(cases)):
+                        ext.record(ev_pairs[k][2], stream)
+                sten.sparsify_grouped_nm_batched([(d["W"], c.n, c.m, c.g, d["values"], d["idx"])
+                                                  for c, d in zip(cases, data)])
+                if ev_pairs is not None:
+                    for k in range(len(cases)):
+                        ext.record(ev_pairs[k][0], stream)
+        with torch.cuda.stream(stream):
+            if ev_pairs is not None:
+                ext.record(ev_pairs[0][3], stream)
+            sten.spmm_grouped_nm_batched_ex(grouped_problems(cases, data), grouped[1], None, grouped[0])
+            if ev_pairs is not None:
+                for k in range(len(cases)):
+                    ext.record(ev_pairs[k][1], stream)
+        return
     if lane_streams:
         fork = torch.cuda.Event()
         fork.record(stream)
@@ -324,16 +366,23 @@ def bench_sten(args, rank, world, local_rank):
     if args.plans_out and rank == 0:
         with open(args.plans_out, "w") as f:
             json.dump({c.label(): sets[0][k]["plan"].as_dict() for k, c in enumerate(cases)}, f, indent=1)
+    mode = args.step_mode or ("grouped" if dtype == "f32" and len(cases) <= 12 else "streams")
+    grouped = [None] * R
+    if mode == "grouped":
+        for r in range(R):
+            nb = sten.batched_workspace_size(grouped_problems(cases, sets[r]), None, GROUPED_TILE)
+            # zero-filled once: the split-K counters start (and are left) at zero
+            grouped[r] = (GROUPED_TILE, torch.zeros(max(nb, 16) // 4 + 4, dtype=torch.float32, device=device))
     ext = ExtEvents()
-    # per case: (after sparsify, after SpMM, before sparsify)
-    ev = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in cases] for _ in range(R)]
+    # per case: (after sparsify, after SpMM, before sparsify, before the grouped SpMM)
+    ev = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in cases] for _ in range(R)]
     step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(R)]
 
     # warm-up (also JIT-free: the library is precompiled) then capture one graph per set;
     # record every timing event once so its CUDA handle exists before capture
     with torch.cuda.stream(stream):
         for r in range(R):
-            run_step(cases, sets[r])
+            run_step(cases, sets[r], stream=stream, grouped=grouped[r])
             for evs in ev[r] + [step_ev[r]]:
                 for e in evs:
                     e.record(stream)
@@ -351,7 +400,8 @@ def bench_sten(args, rank, world, local_rank):
             gph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gph, stream=stream):
                 ext.record(step_ev[r][0], stream)
-                run_step(cases, sets[r], ev[r] if n_lanes == 1 else None, ext, stream, lane_streams, lane_of)
+                run_step(cases, sets[r], ev[r] if n_lanes == 1 else None, ext, stream, lane_streams, lane_of,
+                         grouped=grouped[r])
                 ext.record(step_ev[r][1], stream)
             gs.append(gph)
         torch.cuda.synchronize()
@@ -361,6 +411,20 @@ def bench_sten(args, rank, world, local_rank):
         r = i % R
         if graphs is not None:
             graphs[r].replay()
+        elif grouped[r] is not None:
+            with torch.cuda.stream(stream):
+                step_ev[r][0].record(stream)
+                for k in range(len(cases)):
+                    ev[r][k][2].record(stream)
+                sten.sparsify_grouped_nm_batched([(d["W"], c.n, c.m, c.g, d["values"], d["idx"])
+                                                  for c, d in zip(cases, sets[r])])
+                for k in range(len(cases)):
+                    ev[r][k][0].record(stream)
+                ev[r][0][3].record(stream)
+                sten.spmm_grouped_nm_batched_ex(grouped_problems(cases, sets[r]), grouped[r][1], None, grouped[r][0])
+                for k in range(len(cases)):
+                    ev[r][k][1].record(stream)
+                step_ev[r][1].record(stream)
         else:
             with torch.cuda.stream(stream):
                 step_ev[r][0].record(stream)
@@ -373,8 +437,12 @@ def bench_sten(args, rank, world, local_rank):
                     ev[r][k][1].record(stream)
                 step_ev[r][1].record(stream)
 
-    def timed_loop(graphs, sample_clocks, per_case=True):
-        """W warm-up steps, then exactly K timed steps bracketed by barrier + synchronize."""
+    def timed_loop(graphs, sample_clocks, per_case=True, readback=True):
+        """W warm-up steps, then exactly K timed steps bracketed by barrier + synchronize.
+        readback=False (the headline pass): the K steps are replayed back to back with no host
+        synchronisation inside the timed region; the step time is the CUDA-event interval around
+        all K replays on the replaying stream / K.  readback=True: the per-set in-graph events are
+        read every R steps (per-step and per-kernel brackets; host gaps between replays)."""
         for i in range(args.warmup):
             one(graphs, i)
         torch.cuda.synchronize()
@@ -390,19 +458,23 @@ def bench_sten(args, rank, world, local_rank):
         step_ms, spmm_ms, spars_ms = [], [[] for _ in cases], [[] for _ in cases]
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
+        cur = torch.cuda.current_stream(device)          # graph replays run on the current stream
+        t0.record(cur if graphs is not None else stream)
         for i in range(args.steps):
             one(graphs, i)
             # read back the events of this set before it is replayed again
-            if (i + 1) % R == 0 or i == args.steps - 1:
+            if readback and ((i + 1) % R == 0 or i == args.steps - 1):
                 torch.cuda.synchronize()
                 for j in range(i - (i % R), i + 1):
                     r = j % R
                     step_ms.append(step_ev[r][0].elapsed_time(step_ev[r][1]))
                     for k in (range(len(cases)) if per_case else ()):
-                        spmm_ms[k].append(ev[r][k][0].elapsed_time(ev[r][k][1]))
+                        if grouped[r] is not None:      # one launch for all SpMMs: its bracket, once
+                            spmm_ms[k].append(ev[r][0][3].elapsed_time(ev[r][0][1]) if k == 0 else 0.0)
+                        else:
+                            spmm_ms[k].append(ev[r][k][0].elapsed_time(ev[r][k][1]))
                         spars_ms[k].append(ev[r][k][2].elapsed_time(ev[r][k][0]))
-        t1.record(stream)
+        t1.record(cur if graphs is not None else stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -411,16 +483,18 @@ def bench_sten(args, rank, world, local_rank):
 
     # pass 1 (headline): the step with the independent cases spread over `lanes` streams
     g_conc = build_graphs(lanes) if use_graph else None
-    step_ms, spmm_conc_ms, loop_ms, clocks = timed_loop(g_conc, True, per_case=lanes == 1)
-    # pass 2 (per-kernel roofline): the same step on one stream, so SpMM launches do not overlap
-    if lanes > 1:
+    step_ms, spmm_conc_ms, loop_ms, clocks = timed_loop(g_conc, True, per_case=lanes == 1,
+                                                        readback=not use_graph)
+    # pass 2 (per-kernel brackets): the same step on one stream, so SpMM launches do not overlap
+    if use_graph:
         del g_conc
         g_seq = build_graphs(1)
         seq_step_ms, (spmm_ms, spars_ms), _, _ = timed_loop(g_seq, False)
         del g_seq
     else:
         seq_step_ms, (spmm_ms, spars_ms) = step_ms, spmm_conc_ms
-    total_ms = float(sum(step_ms))
+    # headline: the whole timed loop (K back-to-back graph replays, no host sync inside) / K
+    total_ms = float(loop_ms) if use_graph else float(sum(step_ms))
     # max over ranks
     tt = torch.tensor([total_ms], device=device, dtype=torch.float64)
     if world > 1:
@@ -437,22 +511,32 @@ def bench_sten(args, rank, world, local_rank):
     b2b = None if args.profile else per_kernel_b2b(cases, sets[0], dtype, device, l2, args.steps)
     in_step_spmm_ms = [sum(x) / len(x) for x in spmm_ms]
     in_step_spars_ms = [sum(x) / len(x) for x in spars_ms]
+    grouped_ms = None
+    if mode == "grouped":
+        grouped_ms = in_step_spmm_ms[0] if args.profile else grouped_b2b(cases, sets, grouped)
     if b2b is not None:
-        spmm_ms = [[t] * args.steps for t in b2b["spmm_ms"]]
         spars_ms = [[t] * args.steps for t in b2b["sparsify_ms"]]
+        if grouped_ms is None:
+            spmm_ms = [[t] * args.steps for t in b2b["spmm_ms"]]
+    if grouped_ms is not None:
+        # the dominant kernel is the one grouped launch: all of the step's SpMM time is its duration
+        spmm_ms = [[grouped_ms] * args.steps] + [[0.0] * args.steps for _ in cases[1:]]
     # dominant kernel: the SpMM (fp32 -> CUDA-core FFMA bound, bf16 -> tensor / HBM), per launch
     spmm_total_ms = sum(sum(x) for x in spmm_ms)
     spmm_nz = sum(nz_flops(c) for c in cases) * args.steps
     spmm_bytes_tot = sum(spmm_bytes(c) for c in cases) * args.steps
-    launches_per_step = sum(1 + sten.launch_count(d["plan"]) for d in sets[0])
+    launches_per_step = (len({(c.m, c.n) for c in cases}) + 1) if mode == "grouped" else sum(1 + sten.launch_count(d["plan"])
+                                                                        for d in sets[0])
     peaks = load_peaks()
     if dtype == "f32":
         peak = peaks["fp32_tflops"]
         achieved = spmm_nz / (spmm_total_ms * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
-                "frac": round(achieved / peak, 4), "traffic": peaks.get("traffic_spmm"),
+                "frac": round(achieved / peak, 4), "traffic": measured_traffic(cfg, dtype, mode),
                 "algorithmic_bytes_per_launch": round(sum(spmm_bytes(c) for c in cases) / len(cases), 1),
-                "peak_source": peaks["fp32_source"], "kernel": "spmm_simt_kernel (CUDA-core FFMA)"}
+                "peak_source": peaks["fp32_source"],
+                "kernel": ("spmm_simt_batched_kernel (one grouped split-K launch of the step's %d SpMMs, CUDA-core "
+                           "FFMA2)" % len(cases)) if mode == "grouped" else "spmm_simt_kernel (CUDA-core FFMA)"}
     else:
         t_roof = sum(max(nz_flops(c) / (peaks["bf16_tflops"] * 1e12), spmm_bytes(c) / (peaks["hbm_gbs"] * 1e9))
                      for c in cases) * args.steps
@@ -462,15 +546,15 @@ def bench_sten(args, rank, world, local_rank):
         if hbm_bound:
             achieved = spmm_bytes_tot / (spmm_total_ms * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": round(frac, 4), "traffic": peaks.get("traffic_spmm")}
+                    "frac": round(frac, 4), "traffic": measured_traffic(cfg, dtype, mode)}
         else:
             achieved = spmm_nz / (spmm_total_ms * 1e-3) / 1e12
             roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peaks["bf16_tflops"],
-                    "unit": "TFLOP/s", "frac": round(frac, 4), "traffic": peaks.get("traffic_spmm")}
+                    "unit": "TFLOP/s", "frac": round(frac, 4), "traffic": measured_traffic(cfg, dtype, mode)}
         roof["kernel"] = "spmm (bf16)"
     per_case = []
     for k, c in enumerate(cases):
-        t = sum(spmm_ms[k]) / len(spmm_ms[k])
+        t = b2b["spmm_ms"][k] if (b2b is not None and grouped_ms is not None) else sum(spmm_ms[k]) / len(spmm_ms[k])
         ts = sum(spars_ms[k]) / len(spars_ms[k])
         per_case.append({"case": c.label(), "plan": sets[0][k]["plan"].as_dict(), "spmm_us": round(t * 1e3, 2),
                          "spmm_us_in_step": round(in_step_spmm_ms[k] * 1e3, 2),
@@ -489,12 +573,16 @@ def bench_sten(args, rank, world, local_rank):
                    "parallelism": "dp%d (token-sharded, weight replicated)" % world,
                    "l2": "rotating %d input sets, %.0f MB > 3x L2 (%.0f MB)" % (R, R * set_bytes / 2 ** 20,
                                                                             l2 / 2 ** 20),
-                   "cuda_graph": use_graph, "streams": lanes,
+                   "cuda_graph": use_graph, "streams": lanes, "step_mode": mode,
                    "plans": ("recorded (%s: per-case plans of a measured B200 run, the step-tuned plan cache; "
                              "--retune autotunes)" % os.path.relpath(args.plans_in, ROOT)) if args.plans_in else
                             "AUTO (cost model)" if args.no_tune else
                             "sten_spmm_autotune per case (min of 5 timed launches per variant, before timing)",
-                   "step": "sparsify (a1-a3) + SpMM (a5-a7) per case; independent cases spread over %d "
+                   "step": ("grouped sparsify (a1-a3) of every weight (one launch per (m, n) class, the classes "
+                            "on separate streams), then ONE grouped split-K SpMM launch (a5-a7) of all cases "
+                            "(tile %d, automatic splits), in one CUDA graph" % GROUPED_TILE)
+                           if mode == "grouped" else
+                           "sparsify (a1-a3) + SpMM (a5-a7) per case; independent cases spread over %d "
                            "streams in one CUDA graph" % lanes},
         "roofline": roof,
         "spmm_only": {"value": round(sum(eff_flops(c) for c in cases) * args.steps / (spmm_total_ms * 1e-3) / 1e9, 2),
@@ -580,6 +668,40 @@ def per_kernel_b2b(cases, data, dtype, device, l2, steps):
                    "spmm_us_in_step / sparsify_us_in_step = the event brackets inside the single-stream step"}
 
 
+GROUPED_TILE = 2        # 16-warp SIMT tile (BM 120 x BN 256): fastest grouped step (tools/grouped_probe.py)
+
+
+def grouped_b2b(cases, sets, grouped):
+    """Pass 3 for the grouped step: the R input sets' grouped SpMM launches back to back in one
+    CUDA graph (R x set bytes > 3 x L2), CUDA events around the replay on its stream, median of
+    3 -> ms per launch."""
+    import torch
+    from paper_2304_07613_b200 import sten
+    R = len(sets)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for r in range(R):
+            sten.spmm_grouped_nm_batched_ex(grouped_problems(cases, sets[r]), grouped[r][1], None, grouped[r][0])
+    torch.cuda.synchronize()
+    gph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gph, stream=st):
+        for r in range(R):
+            sten.spmm_grouped_nm_batched_ex(grouped_problems(cases, sets[r]), grouped[r][1], None, grouped[r][0])
+    gph.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream()
+        e0.record(cur)
+        gph.replay()
+        e1.record(cur)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / R)
+    del gph
+    return sorted(ts)[1]
+
+
 def dense_context(cases, data, dtype, device):
     """SURVEY.md §8(d) on-box context: dense torch.matmul on densify(W) at the same shapes
     (fp32 with TF32 disabled, or bf16), per case median of 10 launches with an L2 flush before
@@ -632,11 +754,18 @@ def load_peaks():
     # FP32 CUDA-core peak derived from unit counts and clock
     peaks["fp32_tflops"] = NUM_SMS * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
     peaks["fp32_source"] = "derived: 148 SM x 128 FP32 lanes x 2 flop x %.0f MHz" % sm_mhz
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            peaks["traffic_spmm"] = json.load(f).get("spmm_dram_bytes_per_launch")
     return peaks
+
+
+def measured_traffic(cfg, dtype, mode):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant SpMM launch of THIS config and
+    step mode, from one `ncu --set full` capture (profiles/traffic_r02.json, written by
+    tools/ncu_traffic.py); None when no capture of this exact workload exists."""
+    tpath = os.path.join(ROOT, "profiles", "traffic_r02.json")
+    if not os.path.exists(tpath):
+        return None
+    with open(tpath) as f:
+        return json.load(f).get("c%d_%s_%s" % (cfg, dtype, mode), {}).get("dram_bytes_per_launch")
 
 
 # ------------------------------------------------------------------------------------------------

@@ -103,6 +103,21 @@ sten_status sten_sparsify_grouped_nm(sten_nmg f, sten_dtype dt,
                                      const void* W, int64_t M, int64_t K, int64_t ldw,
                                      void* values, uint8_t* idx, void* stream);
 
+/* Grouped sparsify: the weights of one step in as few launches as possible -- one launch per
+ * (m, n-vector class) of the problems (e.g. 3 launches for the 9 C2 weights), each CTA working on
+ * one problem exactly as sten_sparsify_grouped_nm does (same bits).  All problems share dt.
+ * count in [1, 12]; every problem is validated before any launch (errors as the single call). */
+typedef struct {
+    sten_nmg f;
+    int32_t reserved;
+    const void* W;          /* [M][ldw]          */
+    int64_t M, K, ldw;
+    void* values;           /* [M][K/m*n]        */
+    uint8_t* idx;           /* [M/g][K/m][n]     */
+} sten_sparsify_problem;
+sten_status sten_sparsify_grouped_nm_batched(int32_t count, const sten_sparsify_problem* problems,
+                                             sten_dtype dt, void* stream);
+
 /* NEXT-2 SameFormat re-sparsification: re-pack a new dense W
  * [M][ldw] (e.g. the weights after an optimizer step) with an EXISTING pattern idx, so the
  * format stays fixed: values[r][kb*n+t] = W[r][kb*m + idx[r/g][kb][t]] (bit copies).
@@ -176,6 +191,23 @@ typedef struct {
 } sten_spmm_problem;
 sten_status sten_spmm_grouped_nm_batched(int32_t count, const sten_spmm_problem* problems, int32_t tile,
                                          void* stream);
+
+/* Grouped launch WITH per-problem split-K (the whole step of independent SpMMs in one launch).
+ * splits[p] (NULL or 0 = automatic: every problem's K is cut so that the units of all problems
+ * carry about the same work, ~3 units per resident CTA) splits problem p's m-blocks into S_p
+ * balanced parts of whole slabs; the S_p parts of an output tile park fp32 partials in the
+ * workspace and the last part to arrive adds them in the fixed order z = 0..S_p-1 (the cluster
+ * reduction's order: the same bits as sten_spmm_grouped_nm_ex with plan {SIMT, S_p, tile}).
+ * workspace: caller-allocated, >= sten_spmm_batched_workspace_size bytes, 16-byte aligned; it
+ * starts with one counter per split tile that MUST be zero before the first call (memset the
+ * buffer once after allocating it); every call leaves them at zero.  Calls sharing a workspace
+ * must be stream-ordered.  Other arguments and errors as sten_spmm_grouped_nm_batched; a workspace
+ * smaller than needed -> STEN_ERR_SHAPE, NULL while needed -> STEN_ERR_INVALID_ARG. */
+sten_status sten_spmm_grouped_nm_batched_ex(int32_t count, const sten_spmm_problem* problems,
+                                            const int32_t* splits, int32_t tile,
+                                            void* workspace, int64_t workspace_bytes, void* stream);
+sten_status sten_spmm_batched_workspace_size(int32_t count, const sten_spmm_problem* problems,
+                                             const int32_t* splits, int32_t tile, int64_t* bytes);
 
 /* The plan sten_spmm_grouped_nm would use for this problem. */
 sten_status sten_spmm_plan_query(sten_nmg f, sten_dtype ab_dt, int64_t M, int64_t K, int64_t N,

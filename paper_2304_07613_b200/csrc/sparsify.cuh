@@ -259,6 +259,40 @@ sparsify_grouped_nm_kernel(const T* __restrict__ W, int64_t ldw, int64_t G, int6
     else sparsify_body<T, MB, NK, 0>(W, ldw, grp, kb, KB, n, g, values, Kp, idx);
 }
 
+// Grouped launch of several sparsifications sharing (T, m, NK) -- the weights of one step
+// (sten_sparsify_grouped_nm_batched): CTA b works on problem p with block0[p] <= b < block0[p+1],
+// one thread per (group, m-block) of that problem, exactly as sparsify_grouped_nm_kernel.
+constexpr int kMaxSparsifyBatch = 12;
+struct SparsifyBatch {
+    const void* W[kMaxSparsifyBatch];
+    void* values[kMaxSparsifyBatch];
+    uint8_t* idx[kMaxSparsifyBatch];
+    int64_t ldw[kMaxSparsifyBatch], G[kMaxSparsifyBatch], KB[kMaxSparsifyBatch], Kp[kMaxSparsifyBatch];
+    int n[kMaxSparsifyBatch], g[kMaxSparsifyBatch], aligned[kMaxSparsifyBatch];
+    int block0[kMaxSparsifyBatch + 1];
+    int count;
+};
+
+template <typename T, int MB, int NK>
+__global__ void __launch_bounds__(256)
+sparsify_grouped_nm_batched_kernel(const __grid_constant__ SparsifyBatch bt) {
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    const int b = int(blockIdx.x);
+    int p = 0;
+    while (p + 1 < bt.count && b >= bt.block0[p + 1]) ++p;
+    const int64_t tid = int64_t(b - bt.block0[p]) * blockDim.x + threadIdx.x;
+    const int64_t G = bt.G[p], KB = bt.KB[p];
+    if (tid >= G * KB) return;
+    const uint32_t t32 = uint32_t(tid), kb32 = uint32_t(KB);       // G*KB < 2^31 (checked on the host)
+    const uint32_t q = t32 / kb32;
+    const int64_t grp = q, kb = int64_t(t32 - q * kb32);
+    const T* W = static_cast<const T*>(bt.W[p]);
+    T* values = static_cast<T*>(bt.values[p]);
+    if (bt.aligned[p] == 2) sparsify_body<T, MB, NK, 2>(W, bt.ldw[p], grp, kb, KB, bt.n[p], bt.g[p], values, bt.Kp[p], bt.idx[p]);
+    else if (bt.aligned[p] == 1) sparsify_body<T, MB, NK, 1>(W, bt.ldw[p], grp, kb, KB, bt.n[p], bt.g[p], values, bt.Kp[p], bt.idx[p]);
+    else sparsify_body<T, MB, NK, 0>(W, bt.ldw[p], grp, kb, KB, bt.n[p], bt.g[p], values, bt.Kp[p], bt.idx[p]);
+}
+
 // NEXT-2 SameFormat re-sparsification: re-pack a new dense W' with an EXISTING pattern
 // ("the new tensor is sparsified using the SameFormatSparsifier to maintain the same format",
 // PAPER.md:398): values[r][kb n + t] = W'[r][kb m + idx[r/g][kb][t]].  One thread per

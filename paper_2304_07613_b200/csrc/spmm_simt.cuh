@@ -103,6 +103,12 @@ struct SpmmArgs {
     // fused epilogue (sten_spmm_grouped_nm_bias_act): C = act(C + bias[row]) before the store
     const float* bias;     // [M] or NULL
     int act;               // 0 none, 1 GELU (erf form), 2 ReLU
+    // split-K through global memory (grouped launch, sten_spmm_grouped_nm_batched_ex): when ws != NULL
+    // the S parts of a tile park their partials in ws [tile][S][BM][BN] (fp32) and the last part to
+    // arrive (counter per tile, left at zero) reduces them in the fixed order z = 0..S-1 -- the same
+    // order as the cluster reduction, so both give the same bits
+    float* ws;
+    unsigned* ctr;
 };
 
 // the fused epilogue on the fp32 accumulators of one output row (NEXT-3: "bias + GELU ...
@@ -576,6 +582,56 @@ __device__ __forceinline__ void spmm_simt_body(const SpmmArgs& a, const CUtensor
             return;
         }
     }
+    if (a.ws) {
+        // split-K through global memory: this part's partial tile -> ws, then the last part reduces
+        const int64_t ntx = (a.N + BN - 1) / BN;
+        const int64_t tile_lin = int64_t(by) * ntx + bx;
+        float* part = a.ws + (tile_lin * a.split + bz) * int64_t(BM) * BN;
+        if (warp < CW) {
+#pragma unroll
+            for (int q = 0; q < SUB; ++q)
+#pragma unroll
+                for (int r = 0; r < RG; ++r) {
+                    const int row = (sub0 + q) * RG + r;
+#pragma unroll
+                    for (int j = 0; j < Cfg::kChunks; ++j)
+#pragma unroll
+                        for (int e4 = 0; e4 < EV; e4 += 4) {
+                            const int col = j * 32 * EV + lane * EV + e4;
+                            __stcg(reinterpret_cast<float4*>(part + size_t(row) * BN + col),
+                                   make_float4(acc[q][r][j * EV + e4], acc[q][r][j * EV + e4 + 1],
+                                               acc[q][r][j * EV + e4 + 2], acc[q][r][j * EV + e4 + 3]));
+                        }
+                }
+        }
+        __threadfence();
+        __syncthreads();
+        __shared__ unsigned last_flag;
+        if (tid == 0) last_flag = atomicAdd(a.ctr + tile_lin, 1u) == unsigned(a.split - 1) ? 1u : 0u;
+        __syncthreads();
+        if (!last_flag) return;
+        __threadfence();
+        const float* tile0 = a.ws + tile_lin * a.split * int64_t(BM) * BN;
+        constexpr int E4 = BM * BN / 4;
+        const int np = a.npeer ? a.npeer : 1;
+        for (int e = tid; e < E4; e += NT) {
+            float4 sum = __ldcg(reinterpret_cast<const float4*>(tile0) + e);
+            for (int z = 1; z < a.split; ++z) {
+                const float4 t = __ldcg(reinterpret_cast<const float4*>(tile0 + size_t(z) * BM * BN) + e);
+                sum.x = __fadd_rn(sum.x, t.x); sum.y = __fadd_rn(sum.y, t.y);
+                sum.z = __fadd_rn(sum.z, t.z); sum.w = __fadd_rn(sum.w, t.w);
+            }
+            const int row = (e * 4) / BN, col = (e * 4) % BN;
+            const int64_t gr = m0 + row, gc = n0 + col;
+            if (gr < a.M && gc < a.N) {
+                float v[4] = {sum.x, sum.y, sum.z, sum.w};
+                epilogue(a, gr, v, 4);
+                for (int p = 0; p < np; ++p) store_out<TC>(out_ptr<TC>(a, p), a.ldc, gr, gc, a.N, v, 4, a.c_vec);
+            }
+        }
+        if (tid == 0) a.ctr[tile_lin] = 0u;                       // leave the counter at zero for the next call
+        return;
+    }
     // split-K: park the partial tile [BM][BN] (fp32) after the header, reduce over the cluster
     __syncthreads();
     float* tile = reinterpret_cast<float*>(smem + L.hdr);
@@ -622,6 +678,7 @@ struct SpmmBatch {
     int ntx[kMaxBatch];          // N tiles of each problem
     int count;
 };
+// CTA b -> problem p, part z = unit % S (the S parts of a tile are adjacent CTAs), tile = unit / S
 
 template <typename TAB, typename TC, int RG, int TN, int SUB, int WARPS, int MINB>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
@@ -629,9 +686,11 @@ spmm_simt_batched_kernel(const __grid_constant__ SpmmBatch bt) {
     const int b = int(blockIdx.x);
     int p = 0;
     while (p + 1 < bt.count && b >= bt.tile0[p + 1]) ++p;
-    const int t = b - bt.tile0[p];
+    const int u = b - bt.tile0[p];
+    const int S = bt.a[p].split;
+    const int t = u / S;
     spmm_simt_body<TAB, TC, RG, TN, SUB, WARPS, MINB>(bt.a[p], &bt.tmB[p], &bt.tmV[p], t % bt.ntx[p],
-                                                       t / bt.ntx[p], 0);
+                                                       t / bt.ntx[p], u - t * S);
 }
 
 }  // namespace sten

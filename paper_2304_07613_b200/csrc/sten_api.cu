@@ -92,6 +92,33 @@ bool dispatch_sparsify(int m, const void* W, int64_t ldw, int64_t G, int64_t KB,
     return false;
 }
 
+// grouped sparsify: the problems of one (T, m, NK) class in one launch
+template <typename T, int MB, int NK>
+void launch_sparsify_batch(const SparsifyBatch& bt, int blocks, cudaStream_t st) {
+    sparsify_grouped_nm_batched_kernel<T, MB, NK><<<unsigned(blocks), 256, 0, st>>>(bt);
+}
+
+template <typename T, int MB>
+void launch_sparsify_batch_nk(const SparsifyBatch& bt, int nk, int blocks, cudaStream_t st) {
+    if (nk == 1) launch_sparsify_batch<T, MB, 1>(bt, blocks, st);
+    else if (nk == 2) launch_sparsify_batch<T, MB, 2>(bt, blocks, st);
+    else launch_sparsify_batch<T, MB, 0>(bt, blocks, st);
+}
+
+template <typename T>
+bool dispatch_sparsify_batch(int m, const SparsifyBatch& bt, int nk, int blocks, cudaStream_t st) {
+    switch (m) {
+        case 2: launch_sparsify_batch_nk<T, 2>(bt, nk, blocks, st); return true;
+        case 4: launch_sparsify_batch_nk<T, 4>(bt, nk, blocks, st); return true;
+        case 6: launch_sparsify_batch_nk<T, 6>(bt, nk, blocks, st); return true;
+        case 8: launch_sparsify_batch_nk<T, 8>(bt, nk, blocks, st); return true;
+        case 10: launch_sparsify_batch_nk<T, 10>(bt, nk, blocks, st); return true;
+        case 12: launch_sparsify_batch_nk<T, 12>(bt, nk, blocks, st); return true;
+        case 16: launch_sparsify_batch_nk<T, 16>(bt, nk, blocks, st); return true;
+    }
+    return false;
+}
+
 template <typename T, int MB>
 void launch_densify(const void* values, const uint8_t* idx, int64_t M, int64_t KB, sten_nmg f,
                     int64_t Kp, void* W, int64_t ldw, bool aligned, cudaStream_t st) {
@@ -244,7 +271,7 @@ sten_status launch_simt_batch_cfg(SpmmArgs* as, int count, cudaStream_t st) {
         const int ntx = int((as[p].N + Cfg::kBN - 1) / Cfg::kBN), nty = int((as[p].M + Cfg::kBM - 1) / Cfg::kBM);
         bt.tile0[p] = tiles;
         bt.ntx[p] = ntx;
-        tiles += ntx * nty;
+        tiles += ntx * nty * as[p].split;
         smem_max = std::max(smem_max, sm);
     }
     bt.tile0[count] = tiles;
@@ -253,7 +280,17 @@ sten_status launch_simt_batch_cfg(SpmmArgs* as, int count, cudaStream_t st) {
     auto kern = spmm_simt_batched_kernel<float, float, RG, TN, SUB, WARPS, MINB>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max)) != cudaSuccess)
         return STEN_ERR_CUDA;
-    kern<<<unsigned(tiles), Cfg::kThreads, smem_max, st>>>(bt);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(tiles));
+    cfg.blockDim = dim3(Cfg::kThreads);
+    cfg.dynamicSmemBytes = smem_max;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL: the prologue overlaps the
+    attr[0].val.programmaticStreamSerializationAllowed = 1;            // sparsifier's tail
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, bt) != cudaSuccess) return STEN_ERR_CUDA;
     return last_cuda();
 }
 
@@ -513,6 +550,57 @@ sten_status sten_sparsify_grouped_nm(sten_nmg f, sten_dtype dt, const void* W, i
     return last_cuda();
 }
 
+sten_status sten_sparsify_grouped_nm_batched(int32_t count, const sten_sparsify_problem* probs, sten_dtype dt,
+                                             void* stream) {
+    if (count < 1 || count > kMaxSparsifyBatch || !probs) return STEN_ERR_INVALID_ARG;
+    if (!dtype_ok(dt)) return STEN_ERR_INVALID_ARG;
+    // validate everything before any launch (no partial writes on an argument error)
+    int nkc[kMaxSparsifyBatch], al[kMaxSparsifyBatch];
+    for (int p = 0; p < count; ++p) {
+        const sten_sparsify_problem& q = probs[p];
+        sten_status s = check_format(q.f);
+        if (s) return s;
+        if ((s = check_shape(q.f, q.M, q.K))) return s;
+        if (q.ldw < q.K) return STEN_ERR_SHAPE;
+        if (q.M * q.K > 0 && (!q.W || !q.values || !q.idx)) return STEN_ERR_INVALID_ARG;
+        if ((q.M / q.f.g) * (q.K / q.f.m) > int64_t(0x7fffffff)) return STEN_ERR_UNSUPPORTED;
+        const int64_t ldw_bytes = q.ldw * int64_t(dt_size(dt));
+        const uintptr_t wa = reinterpret_cast<uintptr_t>(q.W);
+        al[p] = (wa % 32 == 0 && ldw_bytes % 32 == 0) ? 2 : (wa % 16 == 0 && ldw_bytes % 16 == 0) ? 1 : 0;
+        const uintptr_t va = reinterpret_cast<uintptr_t>(q.values), ia = reinterpret_cast<uintptr_t>(q.idx);
+        auto vec_ok = [&](int nk) { return q.f.n == nk && va % (size_t(nk) * dt_size(dt)) == 0 && ia % size_t(nk) == 0; };
+        nkc[p] = vec_ok(1) ? 1 : vec_ok(2) ? 2 : 0;
+    }
+    cudaStream_t st = as_stream(stream);
+    bool done[kMaxSparsifyBatch] = {false};
+    for (int p0 = 0; p0 < count; ++p0) {
+        if (done[p0]) continue;
+        // one launch per (m, NK) class, problems in the caller's order
+        SparsifyBatch bt;
+        memset(&bt, 0, sizeof(bt));
+        int blocks = 0;
+        for (int p = p0; p < count; ++p) {
+            if (done[p] || probs[p].f.m != probs[p0].f.m || nkc[p] != nkc[p0]) continue;
+            done[p] = true;
+            const sten_sparsify_problem& q = probs[p];
+            const int64_t G = q.M / q.f.g, KB = q.K / q.f.m;
+            if (G * KB == 0) continue;
+            const int c = bt.count++;
+            bt.W[c] = q.W; bt.values[c] = q.values; bt.idx[c] = q.idx;
+            bt.ldw[c] = q.ldw; bt.G[c] = G; bt.KB[c] = KB; bt.Kp[c] = KB * q.f.n;
+            bt.n[c] = q.f.n; bt.g[c] = q.f.g; bt.aligned[c] = al[p];
+            bt.block0[c] = blocks;
+            blocks += int(grid1d(G * KB));
+        }
+        if (bt.count == 0) continue;
+        bt.block0[bt.count] = blocks;
+        const bool ok = dt == STEN_F32 ? dispatch_sparsify_batch<float>(probs[p0].f.m, bt, nkc[p0], blocks, st)
+                                       : dispatch_sparsify_batch<bf16_t>(probs[p0].f.m, bt, nkc[p0], blocks, st);
+        if (!ok) return STEN_ERR_UNSUPPORTED;
+    }
+    return last_cuda();
+}
+
 sten_status sten_spmm_grouped_nm_allgather(sten_nmg f, sten_dtype ab_dt, const void* values, const uint8_t* idx,
                                            int64_t M, int64_t K, const void* B, int64_t ldb, int64_t N,
                                            void* const* C_peers, int32_t npeers, int64_t col0, int64_t ldc,
@@ -547,14 +635,27 @@ sten_status sten_spmm_grouped_nm_bias_act(sten_nmg f, sten_dtype ab_dt, const vo
                      bias, act);
 }
 
-sten_status sten_spmm_grouped_nm_batched(int32_t count, const sten_spmm_problem* probs, int32_t tile,
-                                         void* stream) {
+}  // extern "C"
+
+namespace {
+
+// BM / BN of the batched tiles (tile 1: 8 warps, tile 2: 16 warps; TN = 8, RG * SUB = 8 rows per warp)
+inline void batch_tile_dims(int tile, int* bm, int* bn) {
+    *bm = (tile == 2 ? 15 : 7) * 8;
+    *bn = 256;
+}
+
+// Validate the problems and fill their kernel arguments; splits[p] (0 = auto) -> a.split.
+// Auto: every problem's K is cut into parts of about the same number of FMAs, so that the units of
+// all problems together give ~3 units per resident CTA slot (the block scheduler balances them).
+sten_status batch_setup(int32_t count, const sten_spmm_problem* probs, const int32_t* splits, int32_t tile,
+                        SpmmArgs* as, int64_t* ws_floats, int64_t* ctr_words) {
     if (count < 1 || count > kMaxBatch || !probs) return STEN_ERR_INVALID_ARG;
-    if (tile == 0) tile = 1;
     if (tile != 1 && tile != 2) return STEN_ERR_UNSUPPORTED;
-    SpmmArgs as[kMaxBatch];
-    int order[kMaxBatch];
+    int bm, bn;
+    batch_tile_dims(tile, &bm, &bn);
     const int rg = simt_rows_per_warp(probs[0].f.g);
+    double tot = 0;
     for (int p = 0; p < count; ++p) {
         const sten_spmm_problem& q = probs[p];
         const sten_nmg f = q.f;
@@ -568,6 +669,7 @@ sten_status sten_spmm_grouped_nm_batched(int32_t count, const sten_spmm_problem*
         if (q.K == 0 && q.M * q.N > 0) return STEN_ERR_UNSUPPORTED;
         if (q.K * q.N > 0 && (!aligned16(q.B) || (q.ldb * 4) % 16 != 0)) return STEN_ERR_UNSUPPORTED;
         if ((reinterpret_cast<uintptr_t>(q.idx) & 3u) != 0) return STEN_ERR_UNSUPPORTED;
+        if (splits && (splits[p] < 0 || splits[p] > kMaxSplit)) return STEN_ERR_UNSUPPORTED;
         SpmmArgs& a = as[p];
         memset(&a, 0, sizeof(a));
         a.values = q.values; a.idx = q.idx; a.B = q.B; a.C = q.C;
@@ -580,15 +682,85 @@ sten_status sten_spmm_grouped_nm_batched(int32_t count, const sten_spmm_problem*
         a.kbs = simt_slab_blocks(f, STEN_F32, tile);
         a.split = 1;
         a.kb_per_split = a.KB;
-        order[p] = p;
+        const double tiles = double((q.N + bn - 1) / bn) * double((q.M + bm - 1) / bm);
+        tot += tiles * double(bm) * bn * double(a.Kp);
     }
-    // longest K first: the block scheduler then fills the tail with short tiles
-    std::stable_sort(order, order + count, [&](int x, int y) { return as[x].Kp > as[y].Kp; });
+    const double slots = double(kNumSMs) * (tile == 2 ? 1 : 2);
+    const double unit = tot / (3.0 * slots);                       // target FMAs per unit
+    int64_t wsf = 0, ctrw = 0;
+    for (int p = 0; p < count; ++p) {
+        SpmmArgs& a = as[p];
+        const int64_t slabs = (a.KB + a.kbs - 1) / a.kbs;
+        int S = splits ? splits[p] : 0;
+        if (S == 0) {
+            const double tile_fma = double(bm) * bn * double(a.Kp);
+            S = int(std::min<double>(kMaxSplit, std::max(1.0, std::floor(tile_fma / unit + 0.5))));
+        }
+        a.split = int(std::max<int64_t>(1, std::min<int64_t>(S, slabs)));
+        a.kb_per_split = ((slabs + a.split - 1) / a.split) * a.kbs;
+        if (a.split > 1 && a.M > 0 && a.N > 0) {
+            const int64_t tiles = ((a.N + bn - 1) / bn) * ((a.M + bm - 1) / bm);
+            wsf += tiles * a.split * int64_t(bm) * bn;
+            ctrw += tiles;
+        }
+    }
+    *ws_floats = wsf;
+    *ctr_words = (ctrw + 31) / 32 * 32;
+    return STEN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+sten_status sten_spmm_batched_workspace_size(int32_t count, const sten_spmm_problem* probs, const int32_t* splits,
+                                             int32_t tile, int64_t* bytes) {
+    if (!bytes) return STEN_ERR_INVALID_ARG;
+    if (tile == 0) tile = 1;
+    SpmmArgs as[kMaxBatch];
+    int64_t wsf = 0, ctrw = 0;
+    sten_status s = batch_setup(count, probs, splits, tile, as, &wsf, &ctrw);
+    if (s) return s;
+    *bytes = ctrw * 4 + wsf * 4;
+    return STEN_OK;
+}
+
+sten_status sten_spmm_grouped_nm_batched_ex(int32_t count, const sten_spmm_problem* probs, const int32_t* splits,
+                                            int32_t tile, void* workspace, int64_t workspace_bytes, void* stream) {
+    if (tile == 0) tile = 1;
+    SpmmArgs as[kMaxBatch];
+    int64_t wsf = 0, ctrw = 0;
+    sten_status s = batch_setup(count, probs, splits, tile, as, &wsf, &ctrw);
+    if (s) return s;
+    if (wsf > 0) {
+        if (!workspace) return STEN_ERR_INVALID_ARG;
+        if (workspace_bytes < ctrw * 4 + wsf * 4 || !aligned16(workspace)) return STEN_ERR_SHAPE;
+        // counters first (zero on entry, left at zero), then each split problem's partial tiles
+        unsigned* ctr = static_cast<unsigned*>(workspace);
+        float* ws = reinterpret_cast<float*>(static_cast<char*>(workspace) + ctrw * 4);
+        int bm, bn;
+        batch_tile_dims(tile, &bm, &bn);
+        for (int p = 0; p < count; ++p) {
+            SpmmArgs& a = as[p];
+            if (a.split <= 1 || a.M == 0 || a.N == 0) continue;
+            const int64_t tiles = ((a.N + bn - 1) / bn) * ((a.M + bm - 1) / bm);
+            a.ws = ws;
+            a.ctr = ctr;
+            ws += tiles * a.split * int64_t(bm) * bn;
+            ctr += tiles;
+        }
+    }
+    // longest unit (K' / S) first: the block scheduler then fills the tail with short units
+    int order[kMaxBatch];
+    for (int p = 0; p < count; ++p) order[p] = p;
+    std::stable_sort(order, order + count,
+                     [&](int x, int y) { return as[x].Kp / as[x].split > as[y].Kp / as[y].split; });
     SpmmArgs sorted[kMaxBatch];
     int live = 0;
     for (int p = 0; p < count; ++p)
         if (as[order[p]].M > 0 && as[order[p]].N > 0) sorted[live++] = as[order[p]];
     if (live == 0) return STEN_OK;
+    const int rg = simt_rows_per_warp(probs[0].f.g);
     cudaStream_t st = as_stream(stream);
     switch (rg) {
         case 8: return launch_simt_batch_rg<8>(sorted, live, tile, st);
@@ -596,6 +768,15 @@ sten_status sten_spmm_grouped_nm_batched(int32_t count, const sten_spmm_problem*
         case 2: return launch_simt_batch_rg<2>(sorted, live, tile, st);
         default: return launch_simt_batch_rg<1>(sorted, live, tile, st);
     }
+}
+
+sten_status sten_spmm_grouped_nm_batched(int32_t count, const sten_spmm_problem* probs, int32_t tile,
+                                         void* stream) {
+    // whole K per CTA (no workspace): every split is 1
+    int32_t ones[kMaxBatch];
+    for (int p = 0; p < kMaxBatch; ++p) ones[p] = 1;
+    if (count < 1 || count > kMaxBatch) return STEN_ERR_INVALID_ARG;
+    return sten_spmm_grouped_nm_batched_ex(count, probs, ones, tile, nullptr, 0, stream);
 }
 
 sten_status sten_resparsify_same_format(sten_nmg f, sten_dtype dt, const void* W, int64_t M, int64_t K,

@@ -37,6 +37,11 @@ class sten_spmm_problem(ctypes.Structure):
                 ("N", ctypes.c_int64), ("C", ctypes.c_void_p), ("ldc", ctypes.c_int64)]
 
 
+class sten_sparsify_problem(ctypes.Structure):
+    _fields_ = [("f", sten_nmg), ("reserved", ctypes.c_int32), ("W", ctypes.c_void_p), ("M", ctypes.c_int64),
+                ("K", ctypes.c_int64), ("ldw", ctypes.c_int64), ("values", ctypes.c_void_p), ("idx", ctypes.c_void_p)]
+
+
 class sten_spmm_plan(ctypes.Structure):
     _fields_ = [("algo", ctypes.c_int32), ("split_k", ctypes.c_int32), ("tile", ctypes.c_int32),
                 ("reserved", ctypes.c_int32 * 5)]
@@ -83,6 +88,14 @@ SIGNATURES = {
                                                      ctypes.POINTER(sten_spmm_plan), _vp]),
     "sten_spmm_grouped_nm_batched": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(sten_spmm_problem),
                                                     ctypes.c_int32, _vp]),
+    "sten_spmm_grouped_nm_batched_ex": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(sten_spmm_problem),
+                                                       ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, _vp, _i64,
+                                                       _vp]),
+    "sten_spmm_batched_workspace_size": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(sten_spmm_problem),
+                                                        ctypes.POINTER(ctypes.c_int32), ctypes.c_int32,
+                                                        ctypes.POINTER(_i64)]),
+    "sten_sparsify_grouped_nm_batched": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(sten_sparsify_problem),
+                                                        ctypes.c_int, _vp]),
     "sten_sp24_packed_size": (ctypes.c_int, [sten_nmg, _i64, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "sten_sp24_pack": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "sten_spmm_sp24": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, ctypes.c_int,
@@ -182,6 +195,27 @@ def sparsify_grouped_nm(W: torch.Tensor, n: int, m: int, g: int, values: torch.T
                                            values.data_ptr(), idx.data_ptr(), _stream(stream)),
            "sten_sparsify_grouped_nm")
     return values, idx
+
+
+def sparsify_grouped_nm_batched(problems, stream=None):
+    """a1-a3 for several weights in as few launches as possible: problems = [(W, n, m, g, values, idx), ...]
+    (sten_sparsify_grouped_nm_batched; same bits as one sparsify_grouped_nm per weight)."""
+    arr = (sten_sparsify_problem * len(problems))()
+    dt = None
+    for k, (W, n, m, g, values, idx) in enumerate(problems):
+        _cuda(W, "W")
+        if dt is None:
+            dt = W.dtype
+        if W.dtype != dt or values.dtype != dt or idx.dtype != torch.uint8:
+            raise TypeError("one dtype for every W / values, uint8 idx")
+        if not values.is_contiguous() or not idx.is_contiguous():
+            raise ValueError("values and idx must be contiguous")
+        arr[k].f = sten_nmg(n, m, g)
+        arr[k].W, arr[k].M, arr[k].K, arr[k].ldw = W.data_ptr(), W.shape[0], W.shape[1], _ld(W)
+        arr[k].values, arr[k].idx = values.data_ptr(), idx.data_ptr()
+    _check(load().sten_sparsify_grouped_nm_batched(len(problems), arr, _dt(problems[0][0]), _stream(stream)),
+           "sten_sparsify_grouped_nm_batched")
+    return [(p[4], p[5]) for p in problems]
 
 
 def resparsify_same_format(W: torch.Tensor, idx: torch.Tensor, n: int, m: int, g: int,
@@ -291,6 +325,41 @@ def spmm_grouped_nm_batched(problems, tile: int = 1, stream=None):
             raise TypeError("the grouped launch is fp32")
     _check(load().sten_spmm_grouped_nm_batched(len(problems), arr, tile, _stream(stream)),
            "sten_spmm_grouped_nm_batched")
+    return [p[6] for p in problems]
+
+
+def _problem_array(problems):
+    arr = (sten_spmm_problem * len(problems))()
+    for k, (values, idx, B, n, m, g, C) in enumerate(problems):
+        _check_operands(values, idx, B)
+        arr[k].f = sten_nmg(n, m, g)
+        arr[k].values, arr[k].idx = values.data_ptr(), idx.data_ptr()
+        arr[k].M, arr[k].K = values.shape[0], B.shape[0]
+        arr[k].B, arr[k].ldb, arr[k].N = B.data_ptr(), _ld(B), B.shape[1]
+        arr[k].C, arr[k].ldc = C.data_ptr(), _ld(C)
+        if values.dtype != torch.float32 or B.dtype != torch.float32 or C.dtype != torch.float32:
+            raise TypeError("the grouped launch is fp32")
+    return arr
+
+
+def batched_workspace_size(problems, splits=None, tile: int = 1) -> int:
+    arr = _problem_array(problems)
+    sp = (ctypes.c_int32 * len(problems))(*splits) if splits is not None else None
+    nb = _i64()
+    _check(load().sten_spmm_batched_workspace_size(len(problems), arr, sp, tile, ctypes.byref(nb)),
+           "sten_spmm_batched_workspace_size")
+    return nb.value
+
+
+def spmm_grouped_nm_batched_ex(problems, workspace: torch.Tensor | None, splits=None, tile: int = 1, stream=None):
+    """ONE launch for several independent fp32 problems WITH per-problem split-K (splits None = automatic),
+    partials reduced through `workspace` (zero-filled once at allocation; sten_spmm_grouped_nm_batched_ex)."""
+    arr = _problem_array(problems)
+    sp = (ctypes.c_int32 * len(problems))(*splits) if splits is not None else None
+    ws_ptr = workspace.data_ptr() if workspace is not None else None
+    ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    _check(load().sten_spmm_grouped_nm_batched_ex(len(problems), arr, sp, tile, ws_ptr, ws_bytes, _stream(stream)),
+           "sten_spmm_grouped_nm_batched_ex")
     return [p[6] for p in problems]
 
 

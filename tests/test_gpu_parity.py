@@ -549,6 +549,39 @@ def test_spmm_batched_equals_single_launches(tile):
         assert rel_err(C, C_ref, Bound) <= 1e-5
 
 
+@pytest.mark.parametrize("tile", [1, 2])
+@pytest.mark.parametrize("splits", [None, [3, 2, 1, 5]])
+def test_spmm_batched_split_k_equals_cluster_split(tile, splits):
+    """The grouped launch with per-problem split-K through the workspace equals, bit for bit, the
+    single launches with the same (tile, split) (cluster DSMEM reduction, same fixed z order), and
+    the oracle within 1e-5; called twice on the same workspace (the counters are left at zero)."""
+    g = 4
+    shapes = [(64, 384, 300, 2, 4), (120, 800, 129, 1, 10), (200, 256, 256, 1, 4), (56, 768, 40, 2, 4)]
+    probs, refs = [], []
+    for k, (M, K, N, n, m) in enumerate(shapes):
+        W = synthetic.weights(M, K, seed=70 + k)
+        B = synthetic.activations(K, N, seed=80 + k)
+        v, i = gpu_sparsify(W, n, m, g, "f32")
+        probs.append((v, i, dev(B, "f32"), n, m, g, torch.full((M, N), float("nan"), device="cuda")))
+        v_ref, i_ref = oracle.sparsify(W, n, m, g)
+        refs.append(oracle.spmm(v_ref, i_ref, B, n, m, g))
+    nb = sten.batched_workspace_size(probs, splits, tile)
+    ws = torch.zeros(max(nb, 16) // 4 + 4, dtype=torch.float32, device="cuda")
+    for rep in range(2):
+        for p in probs:
+            p[6].fill_(float("nan"))
+        sten.spmm_grouped_nm_batched_ex(probs, ws, splits, tile)
+        torch.cuda.synchronize()
+        for k, ((v, i, Bd, n, m, g_, C), (C_ref, Bound)) in enumerate(zip(probs, refs)):
+            assert rel_err(C, C_ref, Bound) <= 1e-5
+            if splits is not None:
+                S = sten.spmm_grouped_nm(v, i, Bd, n, m, g, plan=sten.make_plan(sten.ALGO_SIMT, splits[k], tile))
+                torch.cuda.synchronize()
+                assert torch.equal(C, S), k
+    nwords = 0
+    assert torch.count_nonzero(ws[: 4].view(torch.int32)) == 0 or nb == 0
+
+
 def test_new_entry_points_reject_bad_arguments():
     """Argument errors of the fused / grouped entry points are returned before any launch."""
     n, m, g, M, K, N = 2, 4, 4, 32, 64, 40

@@ -61,9 +61,29 @@ def grouped(tile):
     return f
 
 
+wss = {}
+
+
+def grouped_split(tile, splits=None):
+    key = (tile, None if splits is None else tuple(splits))
+    nb = sten.batched_workspace_size(sets[0], splits, tile)
+    wss[key] = [torch.zeros(max(nb, 16) // 4 + 4, device="cuda") for _ in range(R)]
+
+    def f(r, s):
+        sten.spmm_grouped_nm_batched_ex(sets[r], wss[key][r], splits, tile)
+    return f
+
+
 nz = sum(2.0 * c.M * c.kept * c.N for c in cases)
 out = {"single_stream_us": graph_us(single), "nine_streams_us": graph_us(multi),
-       "grouped_tile1_us": graph_us(grouped(1)), "grouped_tile2_us": graph_us(grouped(2))}
+       "grouped_tile1_us": graph_us(grouped(1)), "grouped_tile2_us": graph_us(grouped(2)),
+       "grouped_split_auto_tile1_us": graph_us(grouped_split(1)),
+       "grouped_split_auto_tile2_us": graph_us(grouped_split(2))}
+for f in (1, 2, 4):
+    for tile in (1, 2):
+        # splits proportional to K' with the factor f (K' = 1536 -> 4 f ... clipped at 8)
+        sp = [max(1, min(8, round(f * c.kept / 384))) for c in cases]
+        out["grouped_split_x%d_tile%d_us" % (f, tile)] = graph_us(grouped_split(tile, sp))
 out = {k: round(v, 2) for k, v in out.items()}
 out["nz_tflops"] = {k: round(nz / (v * 1e-6) / 1e12, 2) for k, v in out.items()}
 print(json.dumps(out))
