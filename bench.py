@@ -14,8 +14,11 @@ into grouped n:m) and a5-a7 (the grouped-n:m x dense SpMM).  Default workload
 metric = effective (dense-equivalent) GFLOP/s = sum_cases 2*M*K*N / step time
 (SPEC.md:311 convention).  Under torchrun every rank runs its own batch (weak
 scaling: tokens are independent columns, no collective on this path); value
-= all ranks' flops / max-over-ranks time.  --config 4 runs the column-sharded
-8192^2 x 65536 product with the NCCL all-gather of C instead (strong scaling).
+= all ranks' flops / max-over-ranks time.  --config 4 (C5) / --config 3 (C4)
+shard the tokens of ONE global problem over the ranks and all-gather C
+(--partition token: NCCL all-gather on a side stream, chunk-pipelined;
+--partition fused: the all-gather fused into the SpMM epilogue over NVLink
+peer memory) -- strong scaling, roofline with the NVLink term.
 
 L2 hygiene: the timed loop cycles through R device copies of the inputs whose
 total size exceeds 3x the L2 (config["l2"]).  Each input set's step is one CUDA
@@ -48,8 +51,8 @@ CONFIG_NAMES = {
     0: "C1 tiny grouped 2:4 SpMM 64x64, g=4, 32 tokens",
     1: "C2 BERT-base linears {768x768,768x3072,3072x768} x {2:4,1:4,1:10} x 1024 tokens",
     2: "C3 BERT-large linears {1024x4096,4096x1024} x {1:4,2:8} x 16384 tokens",
-    3: "C4 BERT-base encoder-layer linears (QKV,O,FFN1,FFN2) 2:4 x 32768 tokens",
-    4: "C5 8192x8192 1:8 x 65536 tokens (one GPU's product; the token-sharded all-gather is parallel.TokenShardedSpmm)",
+    3: "C4 BERT-base encoder-layer linears (QKV,O,FFN1,FFN2) 2:4 x 32768 tokens, token-sharded over the ranks",
+    4: "C5 8192x8192 1:8 x 65536 tokens, column-sharded over the ranks + all-gather of C",
 }
 FP32_LANES_PER_SM = 128        # B200 CUDA-core FP32 lanes per SM (guide unit counts)
 NUM_SMS = 148
@@ -77,6 +80,12 @@ def parse_args():
     p.add_argument("--step-mode", choices=["grouped", "streams"], default=None,
                    help="grouped: the step's SpMMs as ONE grouped split-K launch (sten_spmm_grouped_nm_batched_ex, "
                         "default for fp32); streams: one launch per case spread over --lanes streams")
+    p.add_argument("--partition", choices=["none", "token", "fused"], default=None,
+                   help="configs 3/4 (C4/C5): shard the tokens (columns of B) of ONE global problem over the "
+                        "ranks and all-gather C -- 'token': NCCL all-gather on a side stream, chunk-pipelined "
+                        "(parallel.TokenShardedSpmm); 'fused': the all-gather fused into the SpMM epilogue over "
+                        "NVLink peer memory (parallel.FusedAllGatherSpmm); default token for configs 3/4")
+    p.add_argument("--chunks", type=int, default=4, help="all-gather pipeline chunks (--partition token)")
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu legs)")
     p.add_argument("--out", default=None, help="also append the JSON line to this file")
     return p.parse_args()
@@ -614,6 +623,179 @@ def bench_sten(args, rank, world, local_rank):
     return out, cases, host, dtype, g, gpu_out
 
 
+NVLINK_GBS = 770.0      # measured peer copy per direction (B200_PROFILING.md), the all-gather roofline term
+
+
+def bench_partition(args, rank, world, local_rank):
+    """C4 / C5 (BASELINE.json configs[3], [4]): ONE global problem whose tokens (columns of B and C)
+    are sharded over the ranks, the sparse weight replicated, then an all-gather
+    of C so every rank holds the full output -- strong scaling (the total work is fixed).
+    C5: the 8192^2 1:8 weight x 65536 tokens; C4: the 4 encoder-layer linears x 32768 tokens, the
+    all-gather on the layer output (FFN2's C).  Every rank sparsifies the same seeded W (identical
+    bits: P11 needs no broadcast); its B shard is drawn with its own seed.  Timed: K steps back to
+    back (sparsify + SpMM + all-gather), CUDA events on the compute stream, max over ranks; the
+    all-gather alone is timed the same way for the NVLink fraction."""
+    import torch
+    import torch.distributed as dist
+    from paper_2304_07613_b200 import parallel, sten
+    cfg = args.config
+    dtype, g = default_dtype_g(cfg)
+    dtype = args.dtype or dtype
+    g = args.g or g
+    mode = args.partition or "token"
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    sten.load()
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    cases = cases_for(cfg, g, dtype)
+    N_global = cases[0].N
+    n_local = parallel.padded_shard_width(N_global, world)
+    c0, c1 = parallel.shard_range(N_global, world, rank)
+    nl = c1 - c0
+    data = []
+    for ci, c in enumerate(cases):
+        W = synthetic.weights(c.M, c.K, seed=1234 + ci, dtype=c.dtype, k_pad=c.k_pad)
+        Bh = synthetic.activations(c.K, max(nl, 1), seed=1234 + ci + 1000 * rank, dtype=c.dtype, k_pad=c.k_pad)
+        Wt = torch.from_numpy(W.view(np.int16) if dtype == "bf16" else W)
+        Bt = torch.from_numpy(Bh.view(np.int16) if dtype == "bf16" else Bh)
+        if dtype == "bf16":
+            Wt, Bt = Wt.view(torch.bfloat16), Bt.view(torch.bfloat16)
+        Wd = Wt.to(device)
+        Bd = parallel.aligned_rows(Bt.to(device)[:, :nl])
+        vals = torch.empty((c.M, c.kept), dtype=tdt, device=device)
+        idx = torch.empty((c.M // c.g, c.Kp // c.m, c.n), dtype=torch.uint8, device=device)
+        sten.sparsify_grouped_nm(Wd, c.n, c.m, c.g, values=vals, idx=idx)
+        data.append(dict(W=Wd, B=Bd, values=vals, idx=idx, host=(W, Bh)))
+    torch.cuda.synchronize()
+    last = cases[-1]
+    # the global plan of every linear (P11: shards equal the unsharded product bit for bit)
+    plans = [sten.spmm_plan(c.n, c.m, c.g, c.M, c.Kp, N_global, ab_dtype=tdt, c_dtype=tdt) for c in cases]
+    if mode == "fused":
+        if dtype == "bf16":
+            plans = [sten.make_plan(sten.ALGO_SIMT, 1, 1) if p.algo != sten.ALGO_SIMT else p for p in plans]
+        fused = parallel.FusedAllGatherSpmm(data[-1]["values"], data[-1]["idx"], last.n, last.m, last.g, last.Kp,
+                                           N_global, out_dtype=tdt)
+    else:
+        tok = parallel.TokenShardedSpmm(last.M, N_global, tdt, device,
+                                        parallel.sten_compute(data[-1]["values"], data[-1]["idx"], last.n, last.m,
+                                                              last.g, plans[-1], tdt), chunks=args.chunks)
+    outs = [torch.empty((c.M, max(nl, 1)), dtype=tdt, device=device) for c in cases[:-1]]
+    stream = torch.cuda.current_stream(device)
+
+    def step(sparsify=True):
+        for k, (c, d) in enumerate(zip(cases, data)):
+            if sparsify:
+                sten.sparsify_grouped_nm(d["W"], c.n, c.m, c.g, values=d["values"], idx=d["idx"])
+            if k < len(cases) - 1 and nl > 0:
+                sten.spmm_grouped_nm(d["values"], d["idx"], d["B"], c.n, c.m, c.g, out=outs[k], plan=plans[k])
+        if mode == "fused":
+            return fused.forward(data[-1]["B"])
+        return tok.forward_allgather(data[-1]["B"])
+
+    def timed(fn, steps):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    sampler = ClockSampler(local_rank) if (rank == 0 and not args.profile) else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    ms = timed(step, args.steps)
+    clocks = sampler.stop() if sampler else None
+    # the product alone (no all-gather) and the all-gather alone, same timing
+    Cl = torch.empty((last.M, max(nl, 1)), dtype=tdt, device=device)
+
+    def compute_only():
+        for k, (c, d) in enumerate(zip(cases, data)):
+            sten.sparsify_grouped_nm(d["W"], c.n, c.m, c.g, values=d["values"], idx=d["idx"])
+            if nl > 0:
+                sten.spmm_grouped_nm(d["values"], d["idx"], d["B"], c.n, c.m, c.g,
+                                     out=outs[k] if k < len(cases) - 1 else Cl, plan=plans[k])
+    ms_compute = timed(compute_only, args.steps)
+    es = torch.finfo(tdt).bits // 8
+    gathered = torch.empty((world * last.M, n_local), dtype=tdt, device=device)
+    piece = torch.zeros((last.M, n_local), dtype=tdt, device=device)
+
+    def ag_only():
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, piece)
+        else:
+            gathered.copy_(piece)
+    ms_ag = timed(ag_only, args.steps)
+    # parity: the gathered C of the last linear on rank 0's own columns vs the oracle (sampled)
+    C_full = step()
+    torch.cuda.synchronize()
+    parity = None
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        W, Bh = data[-1]["host"]
+        ns = min(256, nl)
+        v_ref, i_ref = oracle.sparsify(W, last.n, last.m, last.g)
+        C_ref, Bound = oracle.spmm(v_ref, i_ref, np.ascontiguousarray(Bh[:, :ns]), last.n, last.m, last.g,
+                                   nthreads=cores())
+        Cg = C_full[:, c0:c0 + ns].float().cpu().numpy().astype(np.float64)
+        err = float(np.max(np.abs(Cg - C_ref) / np.maximum(Bound, 1e-30)))
+        tol = 1e-5 if dtype == "f32" else 2e-2
+        parity = {"what": "gathered C of the last linear, rank 0's first %d token columns vs the oracle" % ns,
+                  "max_rel_err": err, "status": "ok" if err <= tol else "FAIL"}
+    peaks = load_peaks()
+    flops = sum(eff_flops(c) for c in cases)
+    nz_loc = sum(2.0 * c.M * kept_min(c) * nl for c in cases)
+    s = esize(dtype)
+    bytes_loc = sum(c.M * kept_min(c) * s + (c.M // c.g) * (-(-c.K // c.m)) * c.n + c.K * nl * s + c.M * nl * s
+                    for c in cases)
+    peak_c = peaks["fp32_tflops"] if dtype == "f32" else peaks["bf16_tflops"]
+    t_comp = max(nz_loc / (peak_c * 1e12), bytes_loc / (peaks["hbm_gbs"] * 1e9))
+    ag_bytes = (world - 1) / world * last.M * N_global * s       # received per rank
+    t_ag = ag_bytes / (NVLINK_GBS * 1e9)
+    t_roof = t_comp + t_ag
+    out = {
+        "metric": METRIC, "value": round(flops / (ms * 1e-3) / 1e9, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic (seeded N(0,0.02^2) weights replicated, N(0,1) activations drawn per rank shard)",
+        "config": {"workload": CONFIG_NAMES[cfg], "baseline_config_index": cfg, "g": g,
+                   "cases": [c.label() for c in cases], "tokens_global": N_global, "tokens_per_gpu": nl,
+                   "parallelism": "token-sharded x%d (weight replicated), C all-gathered (%s)" % (
+                       world, "NCCL all_gather_into_tensor on a side stream, %d chunks" % args.chunks
+                       if mode == "token" else "fused into the SpMM epilogue over symmetric-memory peer stores"),
+                   "partition": mode, "l2": "inputs larger than L2 (%.0f MB of B per rank)" % (
+                       sum(c.Kp * nl * s for c in cases) / 2 ** 20)},
+        "roofline": {"bound": "alu+nvlink" if dtype == "f32" else "tensor/hbm+nvlink",
+                     "achieved": round(flops / (ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s effective",
+                     "t_roof_ms": round(t_roof * 1e3, 4), "t_compute_roof_ms": round(t_comp * 1e3, 4),
+                     "t_allgather_roof_ms": round(t_ag * 1e3, 4), "frac": round(t_roof / (ms * 1e-3), 4),
+                     "peak": round(peak_c, 2), "nvlink_gbs": NVLINK_GBS, "traffic": None,
+                     "note": "t_roof = max(nz flops / peak, bytes / HBM) per rank + (P-1)/P M N s_C / NVLink"},
+        "compute_ms": round(ms_compute, 5),
+        "allgather": {"ms": round(ms_ag, 5), "bytes_received_per_rank": int(ag_bytes),
+                      "gbs": round(ag_bytes / (ms_ag * 1e-3) / 1e9, 1) if world > 1 else None,
+                      "nvlink_frac": round(ag_bytes / (ms_ag * 1e-3) / 1e9 / NVLINK_GBS, 4) if world > 1 else None,
+                      "what": "dist.all_gather_into_tensor of the last linear's C shards alone (world 1: a copy)"},
+        "gpu_launches": args.steps * (len(cases) + sum(1 + sten.launch_count(pl) for pl in plans[:-1])
+                                      + ((1 + sten.launch_count(plans[-1])) * (args.chunks if mode == "token" else 1))),
+    }
+    if clocks:
+        out["clocks"] = clocks
+    if parity:
+        out["parity_checked"] = parity["status"] == "ok"
+        out["parity"] = parity
+    return out
+
+
 def per_kernel_b2b(cases, data, dtype, device, l2, steps):
     """Per case: R_k back-to-back SpMM launches (and separately sparsify launches) over R_k
     rotating copies of the inputs in one CUDA graph; R_k x (bytes one launch touches) > 3 x L2.
@@ -947,6 +1129,7 @@ def bench_reference(args, rank, world):
 
 def main():
     args = parse_args()
+    import torch.distributed as _d  # noqa: F401
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -962,9 +1145,25 @@ def main():
         return 0
     import torch
     import torch.distributed as dist
-    if world > 1:
+    if world > 1 or (args.config in (3, 4) and args.partition == "fused"):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.config in (3, 4) and (args.partition or "token") != "none":
+        out = bench_partition(args, rank, world, local_rank)
+        if world > 1:
+            dist.barrier()
+        if rank == 0:
+            line = json.dumps(out)
+            print(line, flush=True)
+            if args.out:
+                with open(args.out, "a") as f:
+                    f.write(line + "\n")
+        if world > 1:
+            dist.destroy_process_group()
+        return 0 if out.get("parity_checked", True) else 3
     out, cases, host, dtype, g, gpu_out = bench_sten(args, rank, world, local_rank)
     if not args.profile:
         if not args.no_e2e:
