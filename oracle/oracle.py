@@ -53,6 +53,8 @@ def _load():
         lib.oracle_same_format.argtypes = [ctypes.c_int] * 4 + [_ptr, _i64, _i64, _i64, _ptr, _ptr]
         lib.oracle_nmg_patterns.argtypes = [ctypes.c_int, ctypes.c_int, _ptr]
         lib.oracle_nmg_sparsify.argtypes = [ctypes.c_int] * 4 + [_ptr, _i64, _i64, _i64, _ptr, _ptr]
+        lib.oracle_nmg_sparsify_exchange.argtypes = [ctypes.c_int] * 4 + [_ptr, _i64, _i64, _i64, ctypes.c_int,
+                                                                          _ptr, _ptr]
         lib.oracle_nmg_densify.argtypes = [ctypes.c_int] * 4 + [_ptr, _ptr, _i64, _i64, _ptr, _i64]
         lib.oracle_nmg_spmm.argtypes = [ctypes.c_int] * 4 + [_ptr, _ptr, _i64, _i64, _ptr, _i64, _i64,
                                                              _ptr, _ptr, ctypes.c_int]
@@ -212,6 +214,22 @@ def nmg_sparsify(W: np.ndarray, n: int, m: int, g: int):
     idx = np.zeros((M // m, K // L, L), dtype=np.uint16)
     _check(_load().oracle_nmg_sparsify(n, m, g, _dtype_code(W), _p(W), M, K, K, _p(values), _p(idx)),
            "nmg_sparsify")
+    return values, idx
+
+
+def nmg_sparsify_exchange(W: np.ndarray, n: int, m: int, g: int, init: int = 0):
+    """The paper's GPU conversion, sequential reading DESIGN.md R22: pairwise
+    pattern swaps that raise the pair's magnitude until a pass makes none.  init 0 = column b starts
+    with pattern b / g, 1 = start from the greedy.  Same layout as nmg_sparsify."""
+    W = np.ascontiguousarray(W)
+    M, K = W.shape
+    L = nmg_chunk(n, m, g)
+    if M % m or K % L:
+        raise ValueError("shape (%d, %d) not divisible by m=%d / L=%d" % (M, K, m, L))
+    values = np.zeros((M // m, K // L, L, n), dtype=W.dtype)
+    idx = np.zeros((M // m, K // L, L), dtype=np.uint16)
+    _check(_load().oracle_nmg_sparsify_exchange(n, m, g, _dtype_code(W), _p(W), M, K, K, int(init), _p(values),
+                                                _p(idx)), "nmg_sparsify_exchange")
     return values, idx
 
 

@@ -370,6 +370,76 @@ int oracle_nmg_sparsify(int n, int m, int g, int dtype,
     return 0;
 }
 
+/* The paper's GPU conversion: "Initially, columns are arbitrarily assigned to
+ * groups.  Each thread iterates over the columns in the other sparsity groups and attempts to
+ * exchange the nonzero pattern it is assigned with an alternative nonzero pattern.  If such a swap
+ * improves the overall magnitude for the pair of columns, it is performed atomically.  This
+ * continues until no changes are made."  Written out sequentially (R22): passes over the
+ * pairs (i, j), i < j ascending, of columns holding different patterns; swap when
+ * mag[i][p_j] + mag[j][p_i] > mag[i][p_i] + mag[j][p_j] (the two-term sums in fp64, exact for
+ * fp32 magnitudes); stop after a pass without a swap.  init 0: column b starts with pattern b / g
+ * (the "arbitrary" start); init 1: the greedy assignment of oracle_nmg_sparsify.  Magnitudes and
+ * storage order as the greedy. */
+int oracle_nmg_sparsify_exchange(int n, int m, int g, int dtype,
+                                 const void* W, int64_t M, int64_t K, int64_t ldw, int init,
+                                 void* values, uint16_t* idx)
+{
+    int rc = nmg_check(n, m, g, dtype, M, K);
+    if (rc) return rc;
+    if (ldw < K || (init != 0 && init != 1)) return 2;
+    if (init == 1) {
+        /* start from the greedy result: run it, then read each column's pattern back */
+        rc = oracle_nmg_sparsify(n, m, g, dtype, W, M, K, ldw, values, idx);
+        if (rc) return rc;
+    }
+    const int C = nmg_binom(m, n);
+    const int64_t L = (int64_t)C * g, NC = K / L, RB = M / m;
+    int32_t* pos = (int32_t*)malloc(sizeof(int32_t) * (size_t)C * n);
+    oracle_nmg_patterns(n, m, pos);
+    float* mag = (float*)malloc(sizeof(float) * (size_t)(L * C));
+    int* pat_of = (int*)malloc(sizeof(int) * (size_t)L);
+    for (int64_t rb = 0; rb < RB; ++rb)
+        for (int64_t c = 0; c < NC; ++c) {
+            for (int64_t b = 0; b < L; ++b)
+                for (int p = 0; p < C; ++p) {
+                    float s = 0.0f;
+                    for (int t = 0; t < n; ++t)
+                        s = s + fabsf(widen(dtype, W, (rb * m + pos[p * n + t]) * ldw + c * L + b));
+                    mag[b * C + p] = s;
+                }
+            if (init == 0) {
+                for (int64_t b = 0; b < L; ++b) pat_of[b] = (int)(b / g);
+            } else {
+                for (int64_t s = 0; s < L; ++s) pat_of[idx[(rb * NC + c) * L + s]] = (int)(s / g);
+            }
+            int changed = 1;
+            while (changed) {
+                changed = 0;
+                for (int64_t i = 0; i < L; ++i)
+                    for (int64_t j = i + 1; j < L; ++j) {
+                        int pi = pat_of[i], pj = pat_of[j];
+                        if (pi == pj) continue;
+                        double now = (double)mag[i * C + pi] + (double)mag[j * C + pj];
+                        double swp = (double)mag[i * C + pj] + (double)mag[j * C + pi];
+                        if (swp > now) { pat_of[i] = pj; pat_of[j] = pi; changed = 1; }
+                    }
+            }
+            for (int p = 0; p < C; ++p) {
+                int64_t s = (int64_t)p * g;
+                for (int64_t b = 0; b < L; ++b)
+                    if (pat_of[b] == p) {
+                        int64_t slot = (rb * NC + c) * L + s;
+                        idx[slot] = (uint16_t)b;
+                        for (int t = 0; t < n; ++t)
+                            copy_elem(dtype, values, slot * n + t, W, (rb * m + pos[p * n + t]) * ldw + c * L + b);
+                        ++s;
+                    }
+            }
+        }
+    free(pos); free(mag); free(pat_of);
+    return 0;
+}
+
 int oracle_nmg_densify(int n, int m, int g, int dtype, const void* values, const uint16_t* idx,
                        int64_t M, int64_t K, void* W_out, int64_t ldw)
 {

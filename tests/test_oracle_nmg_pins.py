@@ -163,3 +163,89 @@ def test_n8_product(n, m, g):
 def test_shape_errors():
     with pytest.raises(ValueError):
         oracle.nmg_sparsify(np.zeros((4, 10), np.float32), 2, 4, 1)     # K not a multiple of L = 6
+
+
+# ---------------------------------------------------------------------------------------------
+# X: the paper's GPU conversion by pattern exchange (R22)
+#   X1 structure as N3 (every pattern g times, permutation, ascending groups, bit-copied values)
+#   X2 fixed point: no pair of columns with different patterns gains by swapping (brute force over
+#      every pair of the output assignment, exact integer arithmetic)
+#   X3 monotone: starting from the greedy never lowers the kept L1 (exact on integers)
+#   X4 <= the exhaustive optimum (tiny chunks)
+#   X5 planted assignment recovered from the arbitrary start
+# ---------------------------------------------------------------------------------------------
+def _assignment(i_chunk, g):
+    """column -> pattern id, read off the storage order (slot s holds pattern s // g)."""
+    pat = np.empty(len(i_chunk), int)
+    for s, b in enumerate(i_chunk.tolist()):
+        pat[b] = s // g
+    return pat
+
+
+@pytest.mark.parametrize("n,m,g", NMG)
+@pytest.mark.parametrize("init", [0, 1])
+def test_x1_x2_exchange_structure_and_fixed_point(n, m, g, init):
+    L = oracle.nmg_chunk(n, m, g)
+    M, K = 2 * m, 2 * L
+    W = _int_weights(M, K, seed=3 * n + 5 * m + 7 * g + init)
+    v, i = oracle.nmg_sparsify_exchange(W, n, m, g, init)
+    D = oracle.nmg_densify(v, i, n, m, g, K)
+    mask = D != 0
+    assert np.array_equal(D, np.where(mask, W, 0))
+    order = [tuple(p) for p in oracle.nmg_patterns(n, m)]
+    A = np.abs(W.astype(np.int64))
+    for rb in range(M // m):
+        for c in range(K // L):
+            ids = i[rb, c]
+            assert sorted(ids.tolist()) == list(range(L))
+            pat = _assignment(ids, g)
+            assert all((pat == p).sum() == g for p in range(len(order)))
+            for p in range(len(order)):
+                assert (np.diff(ids[p * g:(p + 1) * g].astype(int)) > 0).all()
+            # magnitudes mag[b][p] (exact integers) and the 2-exchange optimality of the output
+            blk = A[rb * m:(rb + 1) * m, c * L:(c + 1) * L]
+            mag = np.array([[blk[list(order[p]), b].sum() for p in range(len(order))] for b in range(L)])
+            for a in range(L):
+                for b in range(a + 1, L):
+                    pa, pb = pat[a], pat[b]
+                    if pa != pb:
+                        assert mag[a, pb] + mag[b, pa] <= mag[a, pa] + mag[b, pb], (a, b)
+
+
+@pytest.mark.parametrize("n,m,g", NMG)
+@pytest.mark.parametrize("seed", range(3))
+def test_x3_exchange_never_lowers_the_greedy(n, m, g, seed):
+    L = oracle.nmg_chunk(n, m, g)
+    W = _int_weights(2 * m, 3 * L, seed=100 + seed, lo=-9, hi=9, nonzero=False)
+    vg, ig = oracle.nmg_sparsify(W, n, m, g)
+    vx, ix = oracle.nmg_sparsify_exchange(W, n, m, g, 1)
+    eg = np.abs(oracle.nmg_densify(vg, ig, n, m, g, 3 * L).astype(np.float64)).sum()
+    ex = np.abs(oracle.nmg_densify(vx, ix, n, m, g, 3 * L).astype(np.float64)).sum()
+    assert ex >= eg
+
+
+@pytest.mark.parametrize("n,m,g", [(1, 2, 1), (1, 2, 2), (1, 2, 3), (2, 4, 1), (1, 4, 1), (1, 3, 2), (1, 4, 2)])
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("init", [0, 1])
+def test_x4_exchange_vs_exhaustive(n, m, g, seed, init):
+    L = oracle.nmg_chunk(n, m, g)
+    W = _int_weights(m, L, seed=seed * 17 + n + m + g, lo=-5, hi=5, nonzero=False)
+    v, i = oracle.nmg_sparsify_exchange(W, n, m, g, init)
+    kept = np.abs(oracle.nmg_densify(v, i, n, m, g, L).astype(np.float64)).sum()
+    assert kept <= oracle.nmg_brute_best_energy(W, n, m, g) + 1e-9
+
+
+@pytest.mark.parametrize("n,m,g", NMG)
+def test_x5_exchange_recovers_planted_assignment(n, m, g):
+    L = oracle.nmg_chunk(n, m, g)
+    order = [tuple(p) for p in oracle.nmg_patterns(n, m)]
+    rng = np.random.default_rng(11 * n + m + 3 * g)
+    assign = np.repeat(np.arange(len(order)), g)
+    rng.shuffle(assign)
+    W = np.ones((m, L), np.float32)
+    for b in range(L):
+        for r in order[assign[b]]:
+            W[r, b] = 100.0 + b
+    v, i = oracle.nmg_sparsify_exchange(W, n, m, g, 0)
+    expect = [b for p in range(len(order)) for b in range(L) if assign[b] == p]
+    assert i[0, 0].tolist() == expect
