@@ -277,13 +277,27 @@ sten_status sten_sparse_linear_host(sten_nmg f, sten_dtype ab_dt,
  *   Shapes: M % m == 0 and K % L == 0 (else STEN_ERR_SHAPE; the caller pads);
  *   1 <= n < m <= 16, C(m,n) <= 64 and L * C(m,n) <= 2048 (else
  *   STEN_ERR_UNSUPPORTED).  The SpMM is compiled for (n, m) in {1:2, 1:4, 2:4,
- *   1:8} and fp32 / bf16 inputs (fp32 accumulate); other formats convert and
- *   densify but their product returns STEN_ERR_UNSUPPORTED.  Pointers, streams,
+ *   1:8, 3:6, 2:8, 1:10} and fp32 / bf16 inputs (fp32 accumulate); other formats
+ *   convert and densify but their product returns STEN_ERR_UNSUPPORTED.  Pointers, streams,
  *   ownership and error behaviour as for the grouped n:m calls above.
  * --------------------------------------------------------------------------- */
 sten_status sten_nmg_sparsify(sten_nmg f, sten_dtype dt,
                               const void* W, int64_t M, int64_t K, int64_t ldw,
                               void* values, uint16_t* idx, void* stream);
+
+/* sten_nmg_sparsify with a choice of conversion algorithm:
+ *   method 0  the CPU greedy above (= sten_nmg_sparsify);
+ *   method 1  the paper's GPU conversion: columns start with an arbitrary
+ *             assignment (column b -> pattern b / g), then pairs of columns holding different
+ *             patterns swap them whenever that raises the pair's magnitude, until a pass makes
+ *             no swap; the swaps follow the sequential order of DESIGN.md R22 (pairs (i, j),
+ *             i < j ascending; the two-term sums compared in fp64), so the result is deterministic
+ *             and equals the oracle's;
+ *   method 2  the greedy, refined by the same exchange passes (never lower L1 than the greedy).
+ * Layout, shapes and errors as sten_nmg_sparsify; method out of range -> STEN_ERR_INVALID_ARG. */
+sten_status sten_nmg_sparsify_ex(sten_nmg f, sten_dtype dt,
+                                 const void* W, int64_t M, int64_t K, int64_t ldw,
+                                 void* values, uint16_t* idx, int32_t method, void* stream);
 
 /* to dense: W_out [M][ldw], zeros at pruned positions. */
 sten_status sten_nmg_densify(sten_nmg f, sten_dtype dt,

@@ -62,6 +62,7 @@ struct NmgArgs {
     int64_t M, K, NC, RB;   // NC = K / L chunks per row block, RB = M / m row blocks
     int n, m, g, C, L;
     NmgPatterns pat;
+    int method;             // sparsify: 0 greedy, 1 exchange from pattern b / g, 2 greedy + exchange
 };
 
 // ---- conversion: one warp per chunk ------------------------------------------------------------
@@ -133,7 +134,10 @@ nmg_sparsify_kernel(const NmgArgs a) {
     auto kb = [](unsigned long long k) { return int(0xFFFFu - uint32_t((k >> 16) & 0xFFFFu)); };
     auto kp = [](unsigned long long k) { return int(0xFFFFu - uint32_t(k & 0xFFFFu)); };
 
-    if (L <= 32 && C <= 8 && NI > 96) {      // (small chunks: the L-step loop below is cheaper)
+    if (a.method == 1) {
+        // the paper's GPU variant starts from an arbitrary assignment: column b gets pattern b / g
+        for (int b = lane; b < L; b += 32) pat_of[b] = int16_t(b / g);
+    } else if (L <= 32 && C <= 8 && NI > 96) {      // (small chunks: the L-step loop below is cheaper)
         // Round-based exact greedy (L <= 32: lane b owns column b).  The largest acceptable item
         // is always the largest "proposal" (each free column's best not-full pattern), so in a
         // round the warp sorts the proposals (bitonic, descending) and accepts the longest prefix
@@ -238,6 +242,50 @@ nmg_sparsify_kernel(const NmgArgs a) {
         }
     }
     __syncwarp();
+    if (a.method != 0) {
+        // Exchange refinement, the paper's GPU conversion: swap the patterns of two
+        // columns when that raises the pair's magnitude, until no swap is made.  Sequential order of
+        // DESIGN.md R22 (pairs (i, j), i < j ascending, the first improving j taken, then the scan
+        // continues with i's new pattern), computed warp-parallel: the 32 lanes test j0..j0+31 against
+        // i's current pattern and a ballot finds the first improving one -- the same swaps, in the same
+        // order, as the oracle.  Magnitudes: a table [L][C] in the (now unused) key space.
+        float* mag = reinterpret_cast<float*>(key);
+        for (int i = lane; i < NI; i += 32) {
+            const int b = i / C, p = i - b * C;
+            float s = 0.0f;
+            for (int t = 0; t < n; ++t) s = __fadd_rn(s, fabsf(to_f32(sw[spos[p * n + t] * L + b])));
+            mag[i] = s;
+        }
+        __syncwarp();
+        bool changed = true;
+        while (changed) {
+            changed = false;
+            for (int i = 0; i < L; ++i) {
+                int j0 = i + 1;
+                while (j0 < L) {
+                    const int pi = pat_of[i];
+                    const int j = j0 + lane;
+                    bool imp = false;
+                    if (j < L) {
+                        const int pj = pat_of[j];
+                        if (pj != pi) {
+                            const double now = double(mag[i * C + pi]) + double(mag[j * C + pj]);
+                            const double swp = double(mag[i * C + pj]) + double(mag[j * C + pi]);
+                            imp = swp > now;
+                        }
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, imp);
+                    if (!bal) { j0 += 32; continue; }
+                    const int jj = j0 + __ffs(bal) - 1;
+                    __syncwarp();
+                    if (lane == 0) { const int16_t pj = pat_of[jj]; pat_of[jj] = int16_t(pi); pat_of[i] = pj; }
+                    __syncwarp();
+                    changed = true;
+                    j0 = jj + 1;
+                }
+            }
+        }
+    }
     // store: slot = p g + (number of lower columns with the same pattern)
     T* V = static_cast<T*>(a.values);
     const int64_t base = chunk * L;

@@ -73,6 +73,11 @@ sten_status dispatch_nmg_spmm(int n, int m, const NmgSpmmArgs& a, cudaStream_t s
     if (n == 1 && m == 4) return launch_nmg_spmm<TAB, TC, 1, 4>(a, st);
     if (n == 2 && m == 4) return launch_nmg_spmm<TAB, TC, 2, 4>(a, st);
     if (n == 1 && m == 8) return launch_nmg_spmm<TAB, TC, 1, 8>(a, st);
+    // the paper's Fig.-5 format (3:6) and the 75 / 90 % points of the C2 sweep: more
+    // patterns per chunk (20 / 28 / 10) -> a longer straight-line chunk body
+    if (n == 3 && m == 6) return launch_nmg_spmm<TAB, TC, 3, 6>(a, st);
+    if (n == 2 && m == 8) return launch_nmg_spmm<TAB, TC, 2, 8>(a, st);
+    if (n == 1 && m == 10) return launch_nmg_spmm<TAB, TC, 1, 10>(a, st);
     return STEN_ERR_UNSUPPORTED;
 }
 
@@ -90,9 +95,16 @@ extern "C" {
 
 sten_status sten_nmg_sparsify(sten_nmg f, sten_dtype dt, const void* W, int64_t M, int64_t K, int64_t ldw,
                               void* values, uint16_t* idx, void* stream) {
+    return sten_nmg_sparsify_ex(f, dt, W, M, K, ldw, values, idx, 0, stream);
+}
+
+sten_status sten_nmg_sparsify_ex(sten_nmg f, sten_dtype dt, const void* W, int64_t M, int64_t K, int64_t ldw,
+                                 void* values, uint16_t* idx, int32_t method, void* stream) {
     NmgArgs a = {};
     sten_status s = nmg_setup(f, dt, M, K, &a);
     if (s) return s;
+    if (method < 0 || method > 2) return STEN_ERR_INVALID_ARG;
+    a.method = method;
     if (ldw < K) return STEN_ERR_SHAPE;
     if (M * K > 0 && (!W || !values || !idx)) return STEN_ERR_INVALID_ARG;
     if (M == 0 || K == 0) return STEN_OK;
@@ -150,7 +162,8 @@ sten_status sten_nmg_spmm(sten_nmg f, sten_dtype ab_dt, const void* values, cons
     if (!nmg_dtype_ok(c_dt)) return STEN_ERR_INVALID_ARG;
     if (N < 0 || ldb < N || ldc < N) return STEN_ERR_SHAPE;
     if ((M * K > 0 && (!values || !idx)) || (K * N > 0 && !B) || (M * N > 0 && !C)) return STEN_ERR_INVALID_ARG;
-    const bool compiled = (f.n == 1 && (f.m == 2 || f.m == 4 || f.m == 8)) || (f.n == 2 && f.m == 4);
+    const bool compiled = (f.n == 1 && (f.m == 2 || f.m == 4 || f.m == 8 || f.m == 10)) ||
+                          (f.n == 2 && (f.m == 4 || f.m == 8)) || (f.n == 3 && f.m == 6);
     if (!compiled) return STEN_ERR_UNSUPPORTED;
     // idx / values are staged with 4-byte cp.async (L is even for every compiled format)
     if ((reinterpret_cast<uintptr_t>(idx) & 3u) != 0 || (reinterpret_cast<uintptr_t>(values) & 3u) != 0)

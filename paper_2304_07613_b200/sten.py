@@ -72,6 +72,8 @@ SIGNATURES = {
     "sten_sparse_linear_host": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _i64, _i64,
                                                _vp, _i64, ctypes.c_int, _vp, _i64, _vp]),
     "sten_nmg_sparsify": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "sten_nmg_sparsify_ex": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _vp,
+                                            ctypes.c_int32, _vp]),
     "sten_nmg_densify": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "sten_nmg_spmm": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64, _i64,
                                      _vp, _i64, ctypes.c_int, _vp]),
@@ -436,9 +438,13 @@ def nmg_chunk(n: int, m: int, g: int) -> int:
     return math.comb(m, n) * g
 
 
+NMG_GREEDY, NMG_EXCHANGE, NMG_GREEDY_EXCHANGE = 0, 1, 2
+
+
 def nmg_sparsify(W: torch.Tensor, n: int, m: int, g: int, values: torch.Tensor | None = None,
-                 idx: torch.Tensor | None = None, stream=None):
-    """dense W [M][K] -> (values [M/m][K/L][L][n], idx [M/m][K/L][L] int16 bit patterns of uint16)."""
+                 idx: torch.Tensor | None = None, stream=None, method: int = NMG_GREEDY):
+    """dense W [M][K] -> (values [M/m][K/L][L][n], idx [M/m][K/L][L] int16 bit patterns of uint16);
+    method: 0 greedy, 1 the paper's GPU exchange conversion, 2 greedy + exchange (sten_nmg_sparsify_ex)."""
     _cuda(W, "W")
     M, K = W.shape
     L = nmg_chunk(n, m, g)
@@ -446,8 +452,9 @@ def nmg_sparsify(W: torch.Tensor, n: int, m: int, g: int, values: torch.Tensor |
         values = torch.empty((M // m, K // L, L, n), dtype=W.dtype, device=W.device)
     if idx is None:
         idx = torch.empty((M // m, K // L, L), dtype=torch.int16, device=W.device)
-    _check(load().sten_nmg_sparsify(sten_nmg(n, m, g), _dt(W), W.data_ptr(), M, K, _ld(W),
-                                    values.data_ptr(), idx.data_ptr(), _stream(stream)), "sten_nmg_sparsify")
+    _check(load().sten_nmg_sparsify_ex(sten_nmg(n, m, g), _dt(W), W.data_ptr(), M, K, _ld(W),
+                                       values.data_ptr(), idx.data_ptr(), int(method), _stream(stream)),
+           "sten_nmg_sparsify_ex")
     return values, idx
 
 

@@ -14,8 +14,9 @@ from paper_2304_07613_b200 import sten
 
 pytestmark = pytest.mark.gpu
 
-SPMM_SET = [(1, 2, 1), (1, 2, 4), (1, 4, 4), (2, 4, 1), (2, 4, 4), (1, 8, 2), (1, 8, 4)]
-CONVERT_ONLY = [(3, 6, 1), (2, 5, 2), (1, 3, 3), (2, 8, 1)]
+SPMM_SET = [(1, 2, 1), (1, 2, 4), (1, 4, 4), (2, 4, 1), (2, 4, 4), (1, 8, 2), (1, 8, 4),
+            (3, 6, 1), (3, 6, 2), (2, 8, 1), (1, 10, 4)]
+CONVERT_ONLY = [(2, 5, 2), (1, 3, 3), (2, 6, 1)]
 
 
 def dev(x: np.ndarray, dtype: str, ld_multiple: int = 8) -> torch.Tensor:
@@ -118,8 +119,38 @@ def test_nmg_errors():
     with pytest.raises(sten.StenError) as e:
         sten.nmg_sparsify(W[:, :10], 2, 4, 1)                 # K = 10 not a multiple of L = 6
     assert e.value.status == 2
-    W6 = torch.zeros((6, 20), device="cuda")
-    v, i = sten.nmg_sparsify(W6, 3, 6, 1)                    # converts (C(6,3) = 20)
+    W5 = torch.zeros((5, 20), device="cuda")
+    v, i = sten.nmg_sparsify(W5, 2, 5, 2)                    # converts (C(5,2) = 10, L = 20)
     with pytest.raises(sten.StenError) as e:
-        sten.nmg_spmm(v, i, torch.zeros((20, 8), device="cuda"), 3, 6, 1)
-    assert e.value.status == 3                                # no compiled product for 3:6
+        sten.nmg_spmm(v, i, torch.zeros((20, 8), device="cuda"), 2, 5, 2)
+    assert e.value.status == 3                                # no compiled product for 2:5
+    with pytest.raises(sten.StenError) as e:
+        sten.nmg_sparsify(W5, 2, 5, 2, method=3)              # unknown conversion method
+    assert e.value.status == 1
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n,m,g", SPMM_SET + CONVERT_ONLY)
+@pytest.mark.parametrize("method", [1, 2])
+def test_nmg_exchange_conversion_bit_exact(dtype, n, m, g, method):
+    """The paper's GPU conversion (pattern exchange) on the GPU equals the oracle's
+    sequential reading (R22) bit for bit: idx, values and densify."""
+    L = oracle.nmg_chunk(n, m, g)
+    M, K = 3 * m, 4 * L
+    W = synthetic.weights(M, K, seed=n * 31 + m * 7 + g + method, dtype=dtype)
+    v_ref, i_ref = oracle.nmg_sparsify_exchange(W, n, m, g, 0 if method == 1 else 1)
+    v, i = sten.nmg_sparsify(dev(W, dtype), n, m, g, method=method)
+    torch.cuda.synchronize()
+    assert np.array_equal(host(i), i_ref)
+    assert np.array_equal(host(v).view(np.uint8), v_ref.view(np.uint8))
+
+
+@pytest.mark.parametrize("n,m,g", [(2, 4, 4), (1, 4, 4), (3, 6, 2)])
+def test_nmg_exchange_integer_ties(n, m, g):
+    L = oracle.nmg_chunk(n, m, g)
+    W = synthetic.integer_matrix(4 * m, 4 * L, seed=n + m + g + 1, lo=-2, hi=2)
+    for method in (1, 2):
+        v_ref, i_ref = oracle.nmg_sparsify_exchange(W, n, m, g, 0 if method == 1 else 1)
+        v, i = sten.nmg_sparsify(dev(W, "f32"), n, m, g, method=method)
+        torch.cuda.synchronize()
+        assert np.array_equal(host(i), i_ref) and np.array_equal(host(v), v_ref)
