@@ -9,5 +9,5 @@ from .oracle import (  # noqa: F401
     build, lib_path, sparsify, densify, spmm, dense_matmul, energy, max_threads,
     brute_select, nmg_patterns, nmg_chunk, nmg_sparsify, nmg_sparsify_exchange, nmg_densify, nmg_spmm,
     nmg_brute_best_energy,
-    same_format, gelu, bias_act,
+    same_format, sddmm, mask_check, gelu, bias_act,
 )

@@ -55,6 +55,8 @@ def _load():
         lib.oracle_nmg_sparsify.argtypes = [ctypes.c_int] * 4 + [_ptr, _i64, _i64, _i64, _ptr, _ptr]
         lib.oracle_nmg_sparsify_exchange.argtypes = [ctypes.c_int] * 4 + [_ptr, _i64, _i64, _i64, ctypes.c_int,
                                                                           _ptr, _ptr]
+        lib.oracle_sddmm.argtypes = [ctypes.c_int] * 4 + [_ptr, _i64, _i64, _ptr, _i64, _ptr, _ptr, _ptr, ctypes.c_int]
+        lib.oracle_mask_check.argtypes = [ctypes.c_int] * 4 + [_ptr, _i64, _i64, _i64, _ptr, _ptr, _ptr]
         lib.oracle_nmg_densify.argtypes = [ctypes.c_int] * 4 + [_ptr, _ptr, _i64, _i64, _ptr, _i64]
         lib.oracle_nmg_spmm.argtypes = [ctypes.c_int] * 4 + [_ptr, _ptr, _i64, _i64, _ptr, _i64, _i64,
                                                              _ptr, _ptr, ctypes.c_int]
@@ -294,6 +296,35 @@ def same_format(W: np.ndarray, idx: np.ndarray, n: int, m: int, g: int) -> np.nd
     _check(_load().oracle_same_format(n, m, g, _dtype_code(W), _p(W), M, K, K, _p(idx), _p(values)),
            "same_format")
     return values
+
+
+def sddmm(G: np.ndarray, B: np.ndarray, idx: np.ndarray, n: int, m: int, g: int, nthreads: int = 1):
+    """Weight gradient of C = densify(values, idx) @ B in the values layout (NEXT-2 masked linear):
+    dV[r][kb n + t] = sum_c G[r][c] B[kb m + idx[r/g][kb][t]][c] in fp64, and Bound = sum |G||B|."""
+    G = np.ascontiguousarray(G)
+    B = np.ascontiguousarray(B)
+    idx = np.ascontiguousarray(idx, dtype=np.uint8)
+    M, N = G.shape
+    K = B.shape[0]
+    assert B.shape[1] == N and G.dtype == B.dtype
+    dV = np.zeros((M, K // m * n), np.float64)
+    bound = np.zeros_like(dV)
+    _check(_load().oracle_sddmm(n, m, g, _dtype_code(G), _p(G), M, N, _p(B), K, _p(idx), _p(dV), _p(bound),
+                                int(nthreads)), "sddmm")
+    return dV, bound
+
+
+def mask_check(W: np.ndarray, idx: np.ndarray, n: int, m: int, g: int):
+    """Fixed-mask fast path: (SameFormat values of W at idx, #nonzeros of W outside
+    the pattern)."""
+    W = np.ascontiguousarray(W)
+    idx = np.ascontiguousarray(idx, dtype=np.uint8)
+    M, K = W.shape
+    values = np.zeros((M, K // m * n), dtype=W.dtype)
+    out = np.zeros(1, np.int64)
+    _check(_load().oracle_mask_check(n, m, g, _dtype_code(W), _p(W), M, K, K, _p(idx), _p(values), _p(out)),
+           "mask_check")
+    return values, int(out[0])
 
 
 # ---------------------------------------------------------------------------------------------

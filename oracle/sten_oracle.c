@@ -520,3 +520,57 @@ int oracle_same_format(int n, int m, int g, int dtype, const void* W, int64_t M,
             }
     return 0;
 }
+
+
+/* NEXT-2 masked linear, weight gradient in the grouped n:m format (the "(KeepAll, FixedMaskTensor)"
+ * gradient of PAPER.md:606-617; the masked-dense training path of PAPER.md:584-621): for the product
+ * C = densify(values, idx) x B, the gradient of a loss with dL/dC = G [M][N] w.r.t. the stored values
+ * is dV[r][kb*n+t] = sum_c G[r][c] * B[kb*m + idx[r/g][kb][t]][c] -- the dense G B^T sampled at the
+ * kept positions (SDDMM).  Summed in fp64 in ascending c; Bound = sum |G| |B|. */
+int oracle_sddmm(int n, int m, int g, int dtype, const void* Gm, int64_t M, int64_t N, const void* B,
+                 int64_t K, const uint8_t* idx, double* dV, double* Bound, int nthreads)
+{
+    int rc = check_args(n, m, g, dtype, M, K);
+    if (rc) return rc;
+    if (N < 0) return 2;
+    int64_t KB = K / m, Kp = KB * n;
+#ifdef _OPENMP
+    if (nthreads < 1) nthreads = 1;
+#pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1)
+#endif
+    for (int64_t r = 0; r < M; ++r)
+        for (int64_t kb = 0; kb < KB; ++kb)
+            for (int t = 0; t < n; ++t) {
+                int64_t k = kb * m + idx[((r / g) * KB + kb) * n + t];
+                double acc = 0.0, bound = 0.0;
+                for (int64_t c = 0; c < N; ++c) {
+                    double x = (double)widen(dtype, Gm, r * N + c), y = (double)widen(dtype, B, k * N + c);
+                    acc += x * y;
+                    bound += fabs(x) * fabs(y);
+                }
+                dV[r * Kp + kb * n + t] = acc;
+                if (Bound) Bound[r * Kp + kb * n + t] = bound;
+            }
+    return 0;
+}
+
+/* NEXT-2 fixed-mask fast path ("we avoid unnecessary conversions when the nonzero
+ * locations of the initial and replacement tensors match"): the SameFormat values of a new dense W
+ * at the existing pattern idx, and the number of nonzero entries of W OUTSIDE that pattern (0 <=> the
+ * nonzero locations match, so the re-pack is the whole conversion). */
+int oracle_mask_check(int n, int m, int g, int dtype, const void* W, int64_t M, int64_t K, int64_t ldw,
+                      const uint8_t* idx, void* values, int64_t* outside)
+{
+    int rc = oracle_same_format(n, m, g, dtype, W, M, K, ldw, idx, values);
+    if (rc) return rc;
+    int64_t KB = K / m, cnt = 0;
+    for (int64_t r = 0; r < M; ++r)
+        for (int64_t kb = 0; kb < KB; ++kb)
+            for (int j = 0; j < m; ++j) {
+                int kept = 0;
+                for (int t = 0; t < n; ++t) kept |= idx[((r / g) * KB + kb) * n + t] == j;
+                if (!kept && widen(dtype, W, r * ldw + kb * m + j) != 0.0f) ++cnt;
+            }
+    *outside = cnt;
+    return 0;
+}
