@@ -128,6 +128,29 @@ sten_status sten_resparsify_same_format(sten_nmg f, sten_dtype dt,
                                         const void* W, int64_t M, int64_t K, int64_t ldw,
                                         const uint8_t* idx, void* values, void* stream);
 
+/* NEXT-2 fixed-mask fast path ("we avoid unnecessary conversions when the
+ * nonzero locations of the initial and replacement tensors match"): the SameFormat re-pack of a
+ * new dense W at the existing pattern idx (values as sten_resparsify_same_format) AND, in the same
+ * pass, *outside = the number of nonzero entries of W at pruned positions (device int64, 8-byte
+ * aligned; set by the call).  *outside == 0 <=> the nonzero locations match and the re-pack is the
+ * whole conversion; otherwise the caller re-sparsifies.  outside may be NULL (plain SameFormat). */
+sten_status sten_mask_check_repack(sten_nmg f, sten_dtype dt,
+                                   const void* W, int64_t M, int64_t K, int64_t ldw,
+                                   const uint8_t* idx, void* values, int64_t* outside, void* stream);
+
+/* NEXT-2 masked linear, weight gradient in the grouped n:m format (SDDMM; the
+ * "(KeepAll, FixedMaskTensor)" gradient of PAPER.md:606-617): for C = densify(values, idx) x B
+ * and G = dL/dC,
+ *     dV[r][kb*n+t] = sum_c G[r][c] * B[kb*m + idx[r/g][kb][t]][c]
+ *   G [M][ldg] ab_dt, B [K][ldb] ab_dt (N columns each), idx [M/g][K/m][n],
+ *   dV [M][K/m*n] c_dt (overwritten; the values layout).
+ * fp32 accumulation, deterministic order; G, B bases and rows 16-byte
+ * aligned (else STEN_ERR_UNSUPPORTED).  Other errors as the SpMM. */
+sten_status sten_sddmm_grouped_nm(sten_nmg f, sten_dtype ab_dt,
+                                  const void* G, int64_t M, int64_t N, int64_t ldg,
+                                  const void* B, int64_t K, int64_t ldb, const uint8_t* idx,
+                                  void* dV, sten_dtype c_dt, void* stream);
+
 /* a4: grouped n:m -> dense.  W_out [M][ldw] receives zeros at
  * pruned positions and the stored values at kept ones (columns >= K untouched). */
 sten_status sten_densify(sten_nmg f, sten_dtype dt,

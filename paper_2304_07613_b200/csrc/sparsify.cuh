@@ -300,22 +300,36 @@ sparsify_grouped_nm_batched_kernel(const __grid_constant__ SparsifyBatch bt) {
 template <typename T, int MB>
 __global__ void __launch_bounds__(256)
 same_format_grouped_nm_kernel(const T* __restrict__ W, int64_t ldw, int64_t M, int64_t KB, int n, int g,
-                              const uint8_t* __restrict__ idx, T* __restrict__ values, int64_t Kp, int aligned) {
+                              const uint8_t* __restrict__ idx, T* __restrict__ values, int64_t Kp, int aligned,
+                              unsigned long long* __restrict__ outside) {
     const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= M * KB) return;
-    const int64_t r = tid / KB, kb = tid - r * KB;
-    T row[MB];
-    if (aligned == 2) load_block<T, MB>(W + r * ldw + kb * MB, row, 2);
-    else if (aligned == 1) load_block<T, MB>(W + r * ldw + kb * MB, row, 1);
-    else load_block<T, MB>(W + r * ldw + kb * MB, row, 0);
-    const uint8_t* ip = idx + ((r / g) * KB + kb) * n;
-    T* vp = values + r * Kp + kb * n;
-    for (int t = 0; t < n; ++t) {
-        const int j = ip[t];
-        T v = row[0];
+    uint32_t out_cnt = 0;
+    if (tid < M * KB) {
+        const int64_t r = tid / KB, kb = tid - r * KB;
+        T row[MB];
+        if (aligned == 2) load_block<T, MB>(W + r * ldw + kb * MB, row, 2);
+        else if (aligned == 1) load_block<T, MB>(W + r * ldw + kb * MB, row, 1);
+        else load_block<T, MB>(W + r * ldw + kb * MB, row, 0);
+        const uint8_t* ip = idx + ((r / g) * KB + kb) * n;
+        T* vp = values + r * Kp + kb * n;
+        uint32_t kept = 0;
+        for (int t = 0; t < n; ++t) {
+            const int j = ip[t];
+            kept |= 1u << j;
+            T v = row[0];
 #pragma unroll
-        for (int q = 1; q < MB; ++q) v = j == q ? row[q] : v;
-        vp[t] = v;
+            for (int q = 1; q < MB; ++q) v = j == q ? row[q] : v;
+            vp[t] = v;
+        }
+        if (outside) {
+            // fixed-mask check: nonzero entries of W' at pruned positions
+#pragma unroll
+            for (int q = 0; q < MB; ++q) out_cnt += (!(kept >> q & 1u) && to_f32(row[q]) != 0.0f) ? 1u : 0u;
+        }
+    }
+    if (outside) {
+        const uint32_t w = __reduce_add_sync(0xffffffffu, out_cnt);
+        if ((threadIdx.x & 31) == 0 && w) atomicAdd(outside, (unsigned long long)w);
     }
 }
 

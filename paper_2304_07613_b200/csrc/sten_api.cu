@@ -781,6 +781,11 @@ sten_status sten_spmm_grouped_nm_batched(int32_t count, const sten_spmm_problem*
 
 sten_status sten_resparsify_same_format(sten_nmg f, sten_dtype dt, const void* W, int64_t M, int64_t K,
                                         int64_t ldw, const uint8_t* idx, void* values, void* stream) {
+    return sten_mask_check_repack(f, dt, W, M, K, ldw, idx, values, nullptr, stream);
+}
+
+sten_status sten_mask_check_repack(sten_nmg f, sten_dtype dt, const void* W, int64_t M, int64_t K, int64_t ldw,
+                                   const uint8_t* idx, void* values, int64_t* outside, void* stream) {
     sten_status s = check_format(f);
     if (s) return s;
     if (!dtype_ok(dt)) return STEN_ERR_INVALID_ARG;
@@ -788,20 +793,27 @@ sten_status sten_resparsify_same_format(sten_nmg f, sten_dtype dt, const void* W
     if (ldw < K) return STEN_ERR_SHAPE;
     if (M * K > 0 && (!W || !values || !idx)) return STEN_ERR_INVALID_ARG;
     const int64_t KB = K / f.m, Kp = KB * f.n;
-    if (M == 0 || KB == 0) return STEN_OK;
+    if (outside && (reinterpret_cast<uintptr_t>(outside) & 7u) != 0) return STEN_ERR_UNSUPPORTED;
+    if (M == 0 || KB == 0) {
+        if (outside && cudaMemsetAsync(outside, 0, sizeof(int64_t), as_stream(stream)) != cudaSuccess)
+            return STEN_ERR_CUDA;
+        return STEN_OK;
+    }
     const int64_t ldw_bytes = ldw * int64_t(dt_size(dt));
     const uintptr_t wa = reinterpret_cast<uintptr_t>(W);
     const int aligned = (wa % 32 == 0 && ldw_bytes % 32 == 0) ? 2 : (wa % 16 == 0 && ldw_bytes % 16 == 0) ? 1 : 0;
     cudaStream_t st = as_stream(stream);
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(outside);
+    if (cnt && cudaMemsetAsync(cnt, 0, sizeof(int64_t), st) != cudaSuccess) return STEN_ERR_CUDA;
     const unsigned grid = grid1d(M * KB);
 #define STEN_SF_CASE(MBV)                                                                                      \
     case MBV:                                                                                                 \
         if (dt == STEN_F32)                                                                                   \
             same_format_grouped_nm_kernel<float, MBV><<<grid, 256, 0, st>>>(                                  \
-                static_cast<const float*>(W), ldw, M, KB, f.n, f.g, idx, static_cast<float*>(values), Kp, aligned); \
+                static_cast<const float*>(W), ldw, M, KB, f.n, f.g, idx, static_cast<float*>(values), Kp, aligned, cnt); \
         else                                                                                                  \
             same_format_grouped_nm_kernel<bf16_t, MBV><<<grid, 256, 0, st>>>(                                 \
-                static_cast<const bf16_t*>(W), ldw, M, KB, f.n, f.g, idx, static_cast<bf16_t*>(values), Kp, aligned); \
+                static_cast<const bf16_t*>(W), ldw, M, KB, f.n, f.g, idx, static_cast<bf16_t*>(values), Kp, aligned, cnt); \
         break;
     switch (f.m) {
         STEN_SF_CASE(2) STEN_SF_CASE(4) STEN_SF_CASE(6) STEN_SF_CASE(8) STEN_SF_CASE(10) STEN_SF_CASE(12)

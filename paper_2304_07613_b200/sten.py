@@ -98,6 +98,10 @@ SIGNATURES = {
                                                         ctypes.POINTER(_i64)]),
     "sten_sparsify_grouped_nm_batched": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(sten_sparsify_problem),
                                                         ctypes.c_int, _vp]),
+    "sten_mask_check_repack": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _vp, _vp,
+                                              _vp]),
+    "sten_sddmm_grouped_nm": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _i64, _i64,
+                                             _vp, _vp, ctypes.c_int, _vp]),
     "sten_sp24_packed_size": (ctypes.c_int, [sten_nmg, _i64, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "sten_sp24_pack": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "sten_spmm_sp24": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, ctypes.c_int,
@@ -231,6 +235,39 @@ def resparsify_same_format(W: torch.Tensor, idx: torch.Tensor, n: int, m: int, g
                                               idx.data_ptr(), values.data_ptr(), _stream(stream)),
            "sten_resparsify_same_format")
     return values
+
+
+def mask_check_repack(W: torch.Tensor, idx: torch.Tensor, n: int, m: int, g: int,
+                      values: torch.Tensor | None = None, stream=None):
+    """Fixed-mask fast path: (SameFormat values of W at idx, device int64 tensor = #nonzeros of W outside
+    the pattern) in one pass (sten_mask_check_repack)."""
+    _cuda(W, "W")
+    M, K = W.shape
+    if values is None:
+        values = torch.empty((M, K // m * n), dtype=W.dtype, device=W.device)
+    outside = torch.empty((1,), dtype=torch.int64, device=W.device)
+    _check(load().sten_mask_check_repack(sten_nmg(n, m, g), _dt(W), W.data_ptr(), M, K, _ld(W), idx.data_ptr(),
+                                         values.data_ptr(), outside.data_ptr(), _stream(stream)),
+           "sten_mask_check_repack")
+    return values, outside
+
+
+def sddmm_grouped_nm(G: torch.Tensor, B: torch.Tensor, idx: torch.Tensor, n: int, m: int, g: int,
+                     out: torch.Tensor | None = None, out_dtype=None, stream=None) -> torch.Tensor:
+    """dV [M][K/m*n] = (G @ B^T) sampled at the kept positions (the masked linear's weight gradient in the
+    values layout; sten_sddmm_grouped_nm).  G [M][N], B [K][N]."""
+    _cuda(G, "G")
+    _cuda(B, "B")
+    if G.dtype != B.dtype:
+        raise TypeError("G and B must share a dtype")
+    M, N = G.shape
+    K = B.shape[0]
+    if out is None:
+        out = torch.empty((M, K // m * n), dtype=out_dtype or G.dtype, device=G.device)
+    _check(load().sten_sddmm_grouped_nm(sten_nmg(n, m, g), _dt(G), G.data_ptr(), M, N, _ld(G), B.data_ptr(), K,
+                                        _ld(B), idx.data_ptr(), out.data_ptr(), _dt(out), _stream(stream)),
+           "sten_sddmm_grouped_nm")
+    return out
 
 
 def densify(values: torch.Tensor, idx: torch.Tensor, n: int, m: int, g: int, K: int,
