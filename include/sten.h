@@ -128,6 +128,18 @@ sten_status sten_resparsify_same_format(sten_nmg f, sten_dtype dt,
                                         const void* W, int64_t M, int64_t K, int64_t ldw,
                                         const uint8_t* idx, void* values, void* stream);
 
+/* NEXT-3 fused epilogue with a residual (a BERT encoder's x + Linear(x)):
+ *   C = act(densify(values, idx) x B + bias[row]) + R[row][col]
+ * bias [M] fp32 or NULL, act 0 none / 1 GELU (erf) / 2 ReLU, R [M][ldr] of c_dt or NULL (must not
+ * alias C).  The SIMT kernel's epilogue (plan algo AUTO/SIMT); otherwise as
+ * sten_spmm_grouped_nm_bias_act. */
+sten_status sten_spmm_grouped_nm_epilogue(sten_nmg f, sten_dtype ab_dt,
+                                          const void* values, const uint8_t* idx, int64_t M, int64_t K,
+                                          const void* B, int64_t ldb, int64_t N,
+                                          void* C, int64_t ldc, sten_dtype c_dt,
+                                          const float* bias, int32_t act, const void* residual, int64_t ldr,
+                                          const sten_spmm_plan* plan, void* stream);
+
 /* NEXT-2 fixed-mask fast path ("we avoid unnecessary conversions when the
  * nonzero locations of the initial and replacement tensors match"): the SameFormat re-pack of a
  * new dense W at the existing pattern idx (values as sten_resparsify_same_format) AND, in the same

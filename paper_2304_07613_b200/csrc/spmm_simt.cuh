@@ -103,6 +103,8 @@ struct SpmmArgs {
     // fused epilogue (sten_spmm_grouped_nm_bias_act): C = act(C + bias[row]) before the store
     const float* bias;     // [M] or NULL
     int act;               // 0 none, 1 GELU (erf form), 2 ReLU
+    const void* residual;  // [M][ldr] of the C dtype, added after the activation (NEXT-3: x + Linear(x)), or NULL
+    int64_t ldr;
     // split-K through global memory (grouped launch, sten_spmm_grouped_nm_batched_ex): when ws != NULL
     // the S parts of a tile park their partials in ws [tile][S][BM][BN] (fp32) and the last part to
     // arrive (counter per tile, left at zero) reduces them in the fixed order z = 0..S-1 -- the same
@@ -122,6 +124,15 @@ STEN_DEVICE_INLINE void epilogue(const SpmmArgs& a, int64_t row, float* v, int c
         else if (a.act == 2) x = fmaxf(x, 0.0f);
         v[e] = x;
     }
+}
+
+// residual add of the fused epilogue: v[e] += R[row][col + e] (R in the C dtype)
+template <typename TC>
+STEN_DEVICE_INLINE void add_residual(const SpmmArgs& a, int64_t row, int64_t col, float* v, int cnt) {
+    if (!a.residual) return;
+    const TC* R = static_cast<const TC*>(a.residual) + row * a.ldr;
+    for (int e = 0; e < cnt; ++e)
+        if (col + e < a.N) v[e] = __fadd_rn(v[e], to_f32(R[col + e]));
 }
 
 // destination p of the epilogue: C itself, or peer buffer p of the fused all-gather
@@ -296,6 +307,7 @@ STEN_DEVICE_INLINE void cluster_reduce_store(unsigned char* tile_smem, const Spm
         if (gr < a.M && gc < a.N) {
             float v[4] = {s.x, s.y, s.z, s.w};
             epilogue(a, gr, v, 4);
+            add_residual<TC>(a, gr, gc, v, 4);
             for (int p = 0; p < np; ++p) store_out<TC>(out_ptr<TC>(a, p), a.ldc, gr, gc, a.N, v, 4, a.c_vec);
         }
     }
@@ -574,9 +586,11 @@ __device__ __forceinline__ void spmm_simt_body(const SpmmArgs& a, const CUtensor
                         const int64_t row = m0 + int64_t(sub0 + q) * RG + r;
                         if (row >= a.M) continue;
 #pragma unroll
-                        for (int j = 0; j < Cfg::kChunks; ++j)
-                            store_out<TC>(C, a.ldc, row, n0 + int64_t(j) * 32 * EV + lane * EV, a.N,
-                                          &acc[q][r][j * EV], EV, a.c_vec);
+                        for (int j = 0; j < Cfg::kChunks; ++j) {
+                            const int64_t col = n0 + int64_t(j) * 32 * EV + lane * EV;
+                            if (p == 0) add_residual<TC>(a, row, col, &acc[q][r][j * EV], EV);
+                            store_out<TC>(C, a.ldc, row, col, a.N, &acc[q][r][j * EV], EV, a.c_vec);
+                        }
                     }
             }
             return;
@@ -626,6 +640,7 @@ __device__ __forceinline__ void spmm_simt_body(const SpmmArgs& a, const CUtensor
             if (gr < a.M && gc < a.N) {
                 float v[4] = {sum.x, sum.y, sum.z, sum.w};
                 epilogue(a, gr, v, 4);
+                add_residual<TC>(a, gr, gc, v, 4);
                 for (int p = 0; p < np; ++p) store_out<TC>(out_ptr<TC>(a, p), a.ldc, gr, gc, a.N, v, 4, a.c_vec);
             }
         }

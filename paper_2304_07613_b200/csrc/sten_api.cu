@@ -422,7 +422,8 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
                       int64_t K, const void* B, int64_t ldb, int64_t N, void* C, int64_t ldc,
                       sten_dtype c_dt, const sten_spmm_plan* plan_in, cudaStream_t st,
                       void* const* C_peers = nullptr, int npeers = 0, int64_t col0 = 0,
-                      const float* bias = nullptr, int act = 0) {
+                      const float* bias = nullptr, int act = 0, const void* residual = nullptr,
+                      int64_t ldr = 0) {
     sten_status s = check_format(f);
     if (s) return s;
     if (!dtype_ok(ab_dt) || !dtype_ok(c_dt)) return STEN_ERR_INVALID_ARG;
@@ -484,6 +485,8 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
     a.c_vec = aligned16(C) && (ldc * int64_t(sc)) % 16 == 0;
     a.bias = bias;
     a.act = act;
+    a.residual = residual;
+    a.ldr = ldr;
     if (npeers > 0) {
         // fused all-gather: every peer buffer receives this rank's columns [col0, col0 + N)
         a.npeer = npeers;
@@ -509,7 +512,7 @@ sten_status spmm_impl(sten_nmg f, sten_dtype ab_dt, const void* values, const ui
         return s;
     }
 
-    if ((npeers > 0 || bias || act) && plan.algo != STEN_ALGO_SIMT) return STEN_ERR_UNSUPPORTED;
+    if ((npeers > 0 || bias || act || residual) && plan.algo != STEN_ALGO_SIMT) return STEN_ERR_UNSUPPORTED;
     if (plan.algo == STEN_ALGO_TCGEN05) {
         // B slabs are TMA-loaded in groups of 8 m-blocks (K % 8m == 0); values rows by TMA
         // (16-byte aligned base; the row stride K' = n KB is then a multiple of 16 bytes)
@@ -633,6 +636,24 @@ sten_status sten_spmm_grouped_nm_bias_act(sten_nmg f, sten_dtype ab_dt, const vo
     if (M > 0 && N > 0 && K == 0) return STEN_ERR_UNSUPPORTED;       // no fused zero-fill path
     return spmm_impl(f, ab_dt, values, idx, M, K, B, ldb, N, C, ldc, c_dt, &pl, as_stream(stream), nullptr, 0, 0,
                      bias, act);
+}
+
+sten_status sten_spmm_grouped_nm_epilogue(sten_nmg f, sten_dtype ab_dt, const void* values, const uint8_t* idx,
+                                          int64_t M, int64_t K, const void* B, int64_t ldb, int64_t N, void* C,
+                                          int64_t ldc, sten_dtype c_dt, const float* bias, int32_t act,
+                                          const void* residual, int64_t ldr, const sten_spmm_plan* plan,
+                                          void* stream) {
+    if (act < 0 || act > 2) return STEN_ERR_INVALID_ARG;
+    if (residual && ldr < N) return STEN_ERR_SHAPE;
+    if (residual && residual == C) return STEN_ERR_INVALID_ARG;          // outputs must not overlap inputs
+    sten_spmm_plan pl;
+    memset(&pl, 0, sizeof(pl));
+    if (plan) pl = *plan;
+    if (pl.algo == STEN_ALGO_AUTO) pl.algo = STEN_ALGO_SIMT;
+    if (pl.algo != STEN_ALGO_SIMT) return STEN_ERR_UNSUPPORTED;
+    if (M > 0 && N > 0 && K == 0) return STEN_ERR_UNSUPPORTED;
+    return spmm_impl(f, ab_dt, values, idx, M, K, B, ldb, N, C, ldc, c_dt, &pl, as_stream(stream), nullptr, 0, 0,
+                     bias, act, residual, ldr);
 }
 
 }  // extern "C"

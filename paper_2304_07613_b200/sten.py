@@ -102,6 +102,9 @@ SIGNATURES = {
                                               _vp]),
     "sten_sddmm_grouped_nm": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _i64, _i64,
                                              _vp, _vp, ctypes.c_int, _vp]),
+    "sten_spmm_grouped_nm_epilogue": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64,
+                                                     _i64, _vp, _i64, ctypes.c_int, _vp, ctypes.c_int32, _vp, _i64,
+                                                     ctypes.POINTER(sten_spmm_plan), _vp]),
     "sten_sp24_packed_size": (ctypes.c_int, [sten_nmg, _i64, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "sten_sp24_pack": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "sten_spmm_sp24": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, ctypes.c_int,
@@ -420,6 +423,28 @@ def spmm_grouped_nm_bias_act(values: torch.Tensor, idx: torch.Tensor, B: torch.T
         sten_nmg(n, m, g), _dt(values), values.data_ptr(), idx.data_ptr(), M, K, B.data_ptr(), _ld(B), N,
         out.data_ptr(), _ld(out), _dt(out), bias.data_ptr() if bias is not None else None, act,
         ctypes.byref(plan) if plan is not None else None, _stream(stream)), "sten_spmm_grouped_nm_bias_act")
+    return out
+
+
+def spmm_grouped_nm_epilogue(values: torch.Tensor, idx: torch.Tensor, B: torch.Tensor, n: int, m: int, g: int,
+                             bias: torch.Tensor | None = None, act: int = ACT_NONE,
+                             residual: torch.Tensor | None = None, out: torch.Tensor | None = None, out_dtype=None,
+                             plan: sten_spmm_plan | None = None, stream=None) -> torch.Tensor:
+    """C = act(densify(values, idx) @ B + bias[:, None]) + residual, all in the SpMM epilogue."""
+    _check_operands(values, idx, B)
+    M = values.shape[0]
+    K, N = B.shape
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype or values.dtype, device=B.device)
+    if bias is not None and (bias.dtype != torch.float32 or bias.numel() != M or not bias.is_contiguous()):
+        raise ValueError("bias must be a contiguous float32 vector of length M")
+    if residual is not None and (residual.dtype != out.dtype or tuple(residual.shape) != (M, N)):
+        raise ValueError("residual must be [M][N] in the output dtype")
+    _check(load().sten_spmm_grouped_nm_epilogue(
+        sten_nmg(n, m, g), _dt(values), values.data_ptr(), idx.data_ptr(), M, K, B.data_ptr(), _ld(B), N,
+        out.data_ptr(), _ld(out), _dt(out), bias.data_ptr() if bias is not None else None, act,
+        residual.data_ptr() if residual is not None else None, _ld(residual) if residual is not None else 0,
+        ctypes.byref(plan) if plan is not None else None, _stream(stream)), "sten_spmm_grouped_nm_epilogue")
     return out
 
 
