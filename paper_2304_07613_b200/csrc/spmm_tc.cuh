@@ -20,9 +20,9 @@
 //     the shared-memory stage (producer ring) and finally hand D to the epilogue,
 //     which reads it with `tcgen05.ld.32x32b` (lane = token, column = row) and
 //     stores 32 consecutive tokens per row per instruction.
-// CTA = 512 threads: warp 0 producer (cp.async of the swizzled B slab, the values
-// tile and the idx words), warp 1 MMA issuer, warp 2 TMEM allocator, warps 4..15
-// three gather teams; warps 0..3 run the epilogue.  Tile: 256 rows x 128 tokens.
+// CTA = 768 threads: warp 0 B + idx producer (TMA of the swizzled B slab, cp.async of the idx
+// words), warp 3 values producer (TMA), warp 1 MMA issuer, warp 2 TMEM allocator, warps 4..23
+// five gather teams of four warps; warps 0..3 run the epilogue.  Tile: 256 rows x 128 tokens.
 #pragma once
 #include "common.cuh"
 #include "spmm_simt.cuh"   // SpmmArgs, store_out
