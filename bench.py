@@ -569,9 +569,9 @@ def bench_sten(args, rank, world, local_rank):
                          "spmm_us_in_step": round(in_step_spmm_ms[k] * 1e3, 2),
                          "sparsify_us": round(ts * 1e3, 2),
                          "sparsify_us_in_step": round(in_step_spars_ms[k] * 1e3, 2),
-                         "sparsify_gbs": round(sparsify_bytes(c) / (ts * 1e-3) / 1e9, 1),
-                         "spmm_eff_gflops": round(eff_flops(c) / (t * 1e-3) / 1e9, 1),
-                         "spmm_nz_tflops": round(nz_flops(c) / (t * 1e-3) / 1e12, 3)})
+                         "sparsify_gbs": round(sparsify_bytes(c) / (ts * 1e-3) / 1e9, 1) if ts > 0 else None,
+                         "spmm_eff_gflops": round(eff_flops(c) / (t * 1e-3) / 1e9, 1) if t > 0 else None,
+                         "spmm_nz_tflops": round(nz_flops(c) / (t * 1e-3) / 1e12, 3) if t > 0 else None})
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,

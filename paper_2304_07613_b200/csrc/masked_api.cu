@@ -15,13 +15,22 @@ namespace {
 
 inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+template <typename T, typename TC, int RR>
+sten_status launch_sddmm_rr(const SddmmArgs& a, cudaStream_t st) {
+    const SddmmGeom g = sddmm_geom(a.n, a.m, RR, int(sizeof(T)));
+    auto kern = sddmm_grouped_nm_kernel<T, TC, RR>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.smem)) != cudaSuccess)
+        return STEN_ERR_CUDA;
+    dim3 grid(unsigned((a.Kp + g.kpc - 1) / g.kpc), unsigned((a.M + g.rows - 1) / g.rows));
+    kern<<<grid, 256, g.smem, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? STEN_OK : STEN_ERR_CUDA;
+}
+
 template <typename T, typename TC>
 sten_status launch_sddmm(const SddmmArgs& a, int rr, cudaStream_t st) {
-    dim3 grid(unsigned((a.Kp + 15) / 16), unsigned((a.M + 8 * rr - 1) / (8 * rr)));
-    if (rr == 4) sddmm_grouped_nm_kernel<T, TC, 4><<<grid, 256, 0, st>>>(a);
-    else if (rr == 2) sddmm_grouped_nm_kernel<T, TC, 2><<<grid, 256, 0, st>>>(a);
-    else sddmm_grouped_nm_kernel<T, TC, 1><<<grid, 256, 0, st>>>(a);
-    return cudaGetLastError() == cudaSuccess ? STEN_OK : STEN_ERR_CUDA;
+    if (rr == 4) return launch_sddmm_rr<T, TC, 4>(a, st);
+    if (rr == 2) return launch_sddmm_rr<T, TC, 2>(a, st);
+    return launch_sddmm_rr<T, TC, 1>(a, st);
 }
 
 }  // namespace
