@@ -77,7 +77,7 @@ def parse_args():
                    help="ignore the step-tuned plan cache (paper_2304_07613_b200/plans/) and autotune per case")
     p.add_argument("--lanes", type=int, default=9,
                    help="streams the independent cases of a step are spread over (inside the graph)")
-    p.add_argument("--step-mode", choices=["grouped", "streams"], default=None,
+    p.add_argument("--step-mode", choices=["grouped", "streams", "sp24"], default=None,
                    help="grouped: the step's SpMMs as ONE grouped split-K launch (sten_spmm_grouped_nm_batched_ex, "
                         "default for fp32); streams: one launch per case spread over --lanes streams")
     p.add_argument("--partition", choices=["none", "token", "fused"], default=None,
@@ -267,6 +267,22 @@ def run_step(cases, data, ev_pairs=None, ext=None, stream=None, lane_streams=Non
     the sparsifiers on the lanes, then ONE grouped split-K launch of all SpMMs on `stream`."""
     import torch
     from paper_2304_07613_b200 import sten
+    if grouped == "sp24":
+        # bf16 on the 2:4 structured-sparse tensor cores (K6): grouped sparsify, pack, tcgen05.mma.sp
+        with torch.cuda.stream(stream):
+            if ev_pairs is not None:
+                for k in range(len(cases)):
+                    ext.record(ev_pairs[k][2], stream)
+            sten.sparsify_grouped_nm_batched([(d["W"], c.n, c.m, c.g, d["values"], d["idx"])
+                                              for c, d in zip(cases, data)])
+            for k, (c, d) in enumerate(zip(cases, data)):
+                sten.sp24_pack(d["values"], d["idx"], c.n, c.m, c.g, c.Kp, v24=d["v24"], meta=d["meta"])
+                if ev_pairs is not None:
+                    ext.record(ev_pairs[k][0], stream)
+                sten.spmm_sp24(d["v24"], d["meta"], c.M, c.Kp, d["B"], out=d["C"])
+                if ev_pairs is not None:
+                    ext.record(ev_pairs[k][1], stream)
+        return
     if grouped is not None:
         # the step's weights in one grouped sparsify call (one launch per (m, n) class), then the
         # grouped SpMM (programmatic dependent launch: its prologue overlaps the sparsifier's tail)
@@ -375,8 +391,16 @@ def bench_sten(args, rank, world, local_rank):
     if args.plans_out and rank == 0:
         with open(args.plans_out, "w") as f:
             json.dump({c.label(): sets[0][k]["plan"].as_dict() for k, c in enumerate(cases)}, f, indent=1)
-    mode = args.step_mode or ("grouped" if dtype == "f32" and len(cases) <= 12 else "streams")
+    mode = args.step_mode or ("grouped" if dtype == "f32" and len(cases) <= 12 else
+                              "sp24" if dtype == "bf16" and all(sten.sp24_compatible(c.n, c.m) for c in cases)
+                              else "streams")
     grouped = [None] * R
+    if mode == "sp24":
+        for r in range(R):
+            grouped[r] = "sp24"
+            for k, c in enumerate(cases):
+                d = sets[r][k]
+                d["v24"], d["meta"] = sten.sp24_pack(d["values"], d["idx"], c.n, c.m, c.g, c.Kp)
     if mode == "grouped":
         for r in range(R):
             nb = sten.batched_workspace_size(grouped_problems(cases, sets[r]), None, GROUPED_TILE)
@@ -420,6 +444,11 @@ def bench_sten(args, rank, world, local_rank):
         r = i % R
         if graphs is not None:
             graphs[r].replay()
+        elif grouped[r] == "sp24":
+            with torch.cuda.stream(stream):
+                step_ev[r][0].record(stream)
+                run_step(cases, sets[r], stream=stream, grouped="sp24")
+                step_ev[r][1].record(stream)
         elif grouped[r] is not None:
             with torch.cuda.stream(stream):
                 step_ev[r][0].record(stream)
@@ -478,7 +507,7 @@ def bench_sten(args, rank, world, local_rank):
                     r = j % R
                     step_ms.append(step_ev[r][0].elapsed_time(step_ev[r][1]))
                     for k in (range(len(cases)) if per_case else ()):
-                        if grouped[r] is not None:      # one launch for all SpMMs: its bracket, once
+                        if grouped[r] is not None and grouped[r] != "sp24":   # one launch for all SpMMs
                             spmm_ms[k].append(ev[r][0][3].elapsed_time(ev[r][0][1]) if k == 0 else 0.0)
                         else:
                             spmm_ms[k].append(ev[r][k][0].elapsed_time(ev[r][k][1]))
@@ -517,7 +546,8 @@ def bench_sten(args, rank, world, local_rank):
     # over rotating input copies (R_k x bytes > 3 x L2: cold L2), CUDA events around the graph
     # replay on the replaying stream -- a launch's duration without the event-node gaps that the
     # in-step brackets of pass 2 include
-    b2b = None if args.profile else per_kernel_b2b(cases, sets[0], dtype, device, l2, args.steps)
+    b2b = None if args.profile else per_kernel_b2b(cases, sets[0], dtype, device, l2, args.steps,
+                                                   sp24=(mode == "sp24"))
     in_step_spmm_ms = [sum(x) / len(x) for x in spmm_ms]
     in_step_spars_ms = [sum(x) / len(x) for x in spars_ms]
     grouped_ms = None
@@ -534,7 +564,8 @@ def bench_sten(args, rank, world, local_rank):
     spmm_total_ms = sum(sum(x) for x in spmm_ms)
     spmm_nz = sum(nz_flops(c) for c in cases) * args.steps
     spmm_bytes_tot = sum(spmm_bytes(c) for c in cases) * args.steps
-    launches_per_step = (len({(c.m, c.n) for c in cases}) + 1) if mode == "grouped" else sum(1 + sten.launch_count(d["plan"])
+    launches_per_step = (len({(c.m, c.n) for c in cases}) + 1) if mode == "grouped" else \
+        (len({(c.m, c.n) for c in cases}) + 2 * len(cases)) if mode == "sp24" else sum(1 + sten.launch_count(d["plan"])
                                                                         for d in sets[0])
     peaks = load_peaks()
     if dtype == "f32":
@@ -560,7 +591,8 @@ def bench_sten(args, rank, world, local_rank):
             achieved = spmm_nz / (spmm_total_ms * 1e-3) / 1e12
             roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peaks["bf16_tflops"],
                     "unit": "TFLOP/s", "frac": round(frac, 4), "traffic": measured_traffic(cfg, dtype, mode)}
-        roof["kernel"] = "spmm (bf16)"
+        roof["kernel"] = ("spmm_sp24_kernel (bf16 2:4 structured-sparse tcgen05.mma.sp)" if mode == "sp24"
+                          else "spmm (bf16)")
     per_case = []
     for k, c in enumerate(cases):
         t = b2b["spmm_ms"][k] if (b2b is not None and grouped_ms is not None) else sum(spmm_ms[k]) / len(spmm_ms[k])
@@ -587,7 +619,9 @@ def bench_sten(args, rank, world, local_rank):
                              "--retune autotunes)" % os.path.relpath(args.plans_in, ROOT)) if args.plans_in else
                             "AUTO (cost model)" if args.no_tune else
                             "sten_spmm_autotune per case (min of 5 timed launches per variant, before timing)",
-                   "step": ("grouped sparsify (a1-a3) of every weight (one launch per (m, n) class, the classes "
+                   "step": ("grouped sparsify (a1-a3), then per case the 2:4 pack and the K6 sparse tensor-core "
+                            "SpMM (a5-a7), in one CUDA graph") if mode == "sp24" else
+                           ("grouped sparsify (a1-a3) of every weight (one launch per (m, n) class, the classes "
                             "on separate streams), then ONE grouped split-K SpMM launch (a5-a7) of all cases "
                             "(tile %d, automatic splits), in one CUDA graph" % GROUPED_TILE)
                            if mode == "grouped" else
@@ -796,7 +830,7 @@ def bench_partition(args, rank, world, local_rank):
     return out
 
 
-def per_kernel_b2b(cases, data, dtype, device, l2, steps):
+def per_kernel_b2b(cases, data, dtype, device, l2, steps, sp24=False):
     """Per case: R_k back-to-back SpMM launches (and separately sparsify launches) over R_k
     rotating copies of the inputs in one CUDA graph; R_k x (bytes one launch touches) > 3 x L2.
     Returns per-launch ms (median of 3 replays) for every case."""
@@ -816,7 +850,9 @@ def per_kernel_b2b(cases, data, dtype, device, l2, steps):
         res = []
         for which in ("spmm", "sparsify"):
             def launch(i):
-                if which == "spmm":
+                if which == "spmm" and sp24:
+                    sten.spmm_sp24(d["v24"], d["meta"], c.M, c.Kp, Bs[i], out=Cs[i])
+                elif which == "spmm":
                     sten.spmm_grouped_nm(Vs[i], Is[i], Bs[i], c.n, c.m, c.g, out=Cs[i], plan=d["plan"])
                 else:
                     sten.sparsify_grouped_nm(Ws[i], c.n, c.m, c.g, values=Vs[i], idx=Is[i])

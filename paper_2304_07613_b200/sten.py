@@ -551,8 +551,10 @@ def sp24_compatible(n: int, m: int) -> bool:
     return n == 1 or (n == 2 and m % 4 == 0)
 
 
-def sp24_pack(values: torch.Tensor, idx: torch.Tensor, n: int, m: int, g: int, K: int, stream=None):
-    """(values, idx) -> (v24 [M128][K128/2] bf16, meta uint32) for sten_spmm_sp24 (sten_sp24_pack)."""
+def sp24_pack(values: torch.Tensor, idx: torch.Tensor, n: int, m: int, g: int, K: int, stream=None,
+              v24: torch.Tensor | None = None, meta: torch.Tensor | None = None):
+    """(values, idx) -> (v24 [M128][K128/2] bf16, meta uint32) for sten_spmm_sp24 (sten_sp24_pack);
+    v24 / meta may be preallocated (shapes of an earlier call)."""
     _cuda(values, "values")
     if values.dtype != torch.bfloat16 or idx.dtype != torch.uint8:
         raise TypeError("sp24 packs bf16 values with uint8 idx")
@@ -562,8 +564,12 @@ def sp24_pack(values: torch.Tensor, idx: torch.Tensor, n: int, m: int, g: int, K
     _check(lib.sten_sp24_packed_size(sten_nmg(n, m, g), M, K, ctypes.byref(vb), ctypes.byref(mb)),
            "sten_sp24_packed_size")
     M128 = -(-M // 128) * 128
-    v24 = torch.empty((M128, vb.value // 2 // max(M128, 1)), dtype=torch.bfloat16, device=values.device)
-    meta = torch.empty((mb.value // 4,), dtype=torch.int32, device=values.device)
+    if v24 is None:
+        v24 = torch.empty((M128, vb.value // 2 // max(M128, 1)), dtype=torch.bfloat16, device=values.device)
+    if meta is None:
+        meta = torch.empty((mb.value // 4,), dtype=torch.int32, device=values.device)
+    if v24.numel() * 2 < vb.value or meta.numel() * 4 < mb.value:
+        raise ValueError("preallocated v24 / meta too small")
     _check(lib.sten_sp24_pack(sten_nmg(n, m, g), BF16, values.data_ptr(), idx.data_ptr(), M, K, v24.data_ptr(),
                               meta.data_ptr(), _stream(stream)), "sten_sp24_pack")
     return v24, meta
