@@ -385,9 +385,10 @@ sten_status sten_sp24_pack(sten_nmg f, sten_dtype dt, const void* values, const 
                            int64_t M, int64_t K, void* v24, uint32_t* meta, void* stream);
 
 /* C [M][ldc] (c_dt, overwritten) = densify(values, idx) x B, B [K][ldb] bf16
- * (B base, v24 and meta 16-byte aligned, ldb % 8 == 0).  tile: 0 = default,
- * 1 = 256 rows x 128 tokens (3 stages), 2 = 256 x 192, 3 = 384 x 128,
- * 4 = 128 x 256, 5 = 128 x 128 (4 stages).  fp32 accumulation in TMEM over
+ * (B base, v24 and meta 16-byte aligned, ldb % 8 == 0).  tile: 0 = default
+ * (6 when K >= 2048, else 1), 1 = 256 rows x 192 tokens, 2 = 256 x 128,
+ * 3 = 384 x 128, 4 = 128 x 256, 5 = 128 x 128 (one CTA per SM, persistent),
+ * 6 = a CTA pair on two SMs (tcgen05 cta_group::2, 256 x 256 per pair).  fp32 accumulation in TMEM over
  * K in ascending 32-k steps (independent of N and the token tiling). */
 sten_status sten_spmm_sp24(const void* v24, const uint32_t* meta, int64_t M, int64_t K,
                            const void* B, int64_t ldb, int64_t N,

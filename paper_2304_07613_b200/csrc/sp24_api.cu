@@ -82,6 +82,73 @@ sten_status launch_sp24(Sp24Args a, cudaStream_t st) {
     return STEN_OK;
 }
 
+// 2-SM variant (tile 6): clusters of 2 CTAs, 256 x 256 pair tiles, one pair per 2 SMs (persistent)
+template <typename TC, int ST>
+sten_status launch_sp24_2sm(Sp24Args a, cudaStream_t st) {
+    using Cfg = Sp24Cfg2<ST>;
+    CUtensorMap tmA, tmB, tmC, tmE;
+    memset(&tmA, 0, sizeof(tmA));
+    memset(&tmB, 0, sizeof(tmB));
+    memset(&tmC, 0, sizeof(tmC));
+    memset(&tmE, 0, sizeof(tmE));
+    {   // v24 [M128][Kc]: box [128 rows][64 stored k], 128-byte swizzle
+        const uint64_t dims[2] = {uint64_t(a.Kc), uint64_t(sp24_m128(a.M))};
+        const uint64_t strides[1] = {uint64_t(a.Kc) * 2};
+        const uint32_t box[2] = {64u, 128u};
+        if (!make_tmap_nd(&tmA, a.v24, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dims, strides, box,
+                          CU_TENSOR_MAP_SWIZZLE_128B))
+            return STEN_ERR_CUDA;
+    }
+    {   // B [K][ldb]: box [128 k][64 tokens], 128-byte swizzle
+        const uint64_t dims[2] = {uint64_t(a.N), uint64_t(a.K)};
+        const uint64_t strides[1] = {uint64_t(a.ldb) * 2};
+        const uint32_t box[2] = {64u, 128u};
+        if (!make_tmap_nd(&tmB, a.B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dims, strides, box,
+                          CU_TENSOR_MAP_SWIZZLE_128B))
+            return STEN_ERR_CUDA;
+    }
+    {   // C [M][ldc]: TMA store boxes [32 rows][32 tokens]
+        const uint64_t dims[2] = {uint64_t(a.N), uint64_t(a.M)};
+        const uint64_t strides[1] = {uint64_t(a.ldc) * sizeof(TC)};
+        const uint32_t box[2] = {32u, 32u};
+        if (!make_tmap_nd(&tmC, a.C, sizeof(TC) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                          2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
+            return STEN_ERR_CUDA;
+    }
+    {   // metadata image [M128/128 * KT][128 lanes][4 u32]: box {4, 128, 1} = one (block, K-tile) image
+        const uint64_t dims[3] = {4, 128, uint64_t(sp24_m128(a.M) / 128 * a.KT)};
+        const uint64_t strides[2] = {16, 2048};
+        const uint32_t box[3] = {4u, 128u, 1u};
+        if (!make_tmap_nd(&tmE, a.meta, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, dims, strides, box,
+                          CU_TENSOR_MAP_SWIZZLE_NONE))
+            return STEN_ERR_CUDA;
+    }
+    a.row_tiles = int((a.M + Cfg::kBM - 1) / Cfg::kBM);
+    a.col_tiles = int((a.N + Cfg::kBN - 1) / Cfg::kBN);
+    const int ntiles = a.row_tiles * a.col_tiles;
+    auto kern = spmm_sp24_2sm_kernel<TC, ST>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::kSmem)) != cudaSuccess)
+        return STEN_ERR_CUDA;
+    const int pairs = ntiles < num_sms() / 2 ? ntiles : num_sms() / 2;
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(unsigned(2 * pairs));
+    cfg.blockDim = dim3(Cfg::kThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    if (cudaLaunchKernelEx(&cfg, kern, a, tmA, tmB, tmC, tmE) != cudaSuccess) return STEN_ERR_CUDA;
+    return STEN_OK;
+}
+
 template <typename TC>
 sten_status launch_sp24_tile(const Sp24Args& a, int tile, cudaStream_t st) {
     switch (tile) {
@@ -90,6 +157,7 @@ sten_status launch_sp24_tile(const Sp24Args& a, int tile, cudaStream_t st) {
         case 3: return launch_sp24<TC, 3, 128, 4>(a, st);
         case 4: return launch_sp24<TC, 1, 256, 4>(a, st);
         case 5: return launch_sp24<TC, 1, 128, 6>(a, st);
+        case 6: return launch_sp24_2sm<TC, 3>(a, st);
         default: return STEN_ERR_UNSUPPORTED;
     }
 }
@@ -134,8 +202,10 @@ sten_status sten_spmm_sp24(const void* v24, const uint32_t* meta, int64_t M, int
     if (M < 0 || K < 0 || N < 0 || ldb < N || ldc < N) return STEN_ERR_SHAPE;
     if (c_dt != STEN_F32 && c_dt != STEN_BF16) return STEN_ERR_INVALID_ARG;
     if ((M * K > 0 && (!v24 || !meta)) || (K * N > 0 && !B) || (M * N > 0 && !C)) return STEN_ERR_INVALID_ARG;
-    if (tile == 0) tile = 1;
-    if (tile < 1 || tile > 5) return STEN_ERR_UNSUPPORTED;
+    // default: the 2-SM pair kernel when K is long enough to amortise its per-tile epilogue (one D
+    // buffer per pair), else the 256 x 192 1-SM tile (measured on C3)
+    if (tile == 0) tile = K >= 2048 ? 6 : 1;
+    if (tile < 1 || tile > 6) return STEN_ERR_UNSUPPORTED;
     if (K * N > 0 && (!al16(B) || (ldb * 2) % 16 != 0)) return STEN_ERR_UNSUPPORTED;
     if (M * K > 0 && (!al16(v24) || !al16(meta))) return STEN_ERR_UNSUPPORTED;
     if (M * N > 0 && (!al16(C) || (ldc * (c_dt == STEN_F32 ? 4 : 2)) % 16 != 0)) return STEN_ERR_UNSUPPORTED;

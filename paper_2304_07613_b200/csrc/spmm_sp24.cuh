@@ -271,30 +271,50 @@ spmm_sp24_kernel(const Sp24Args a, const __grid_constant__ CUtensorMap tmA, cons
         // ======================= metadata writers =======================
         const int q = warp & 3;
         const int tl = 32 * q + lane;                                  // TMEM lane
-        int g = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        // the metadata words of stage g (this CTA's g-th K-step over its tiles), prefetched PF stages
+        // ahead in registers: the L2 latency of one load per stage would otherwise pace the pipeline
+        constexpr int PF = 8;
+        const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+        const int total = my_tiles * nkt;
+        auto load_stage = [&](int g, uint2 (&w)[MB]) {
+            const int t = int(blockIdx.x) + (g / nkt) * int(gridDim.x), kt = g % nkt;
             const int64_t mb0 = int64_t(t % a.row_tiles) * MB;
-            for (int kt = 0; kt < nkt; ++kt, ++g) {
-                const int s = g % ST;
-                uint2 w[MB];
 #pragma unroll
-                for (int mb = 0; mb < MB; ++mb) {
-                    const int64_t blk = (mb0 + mb) * a.KT + (kt >> 1);
-                    const bool in = (mb0 + mb) * 128 < sp24_m128(a.M) && !(a.exp & 8);
-                    w[mb] = in ? ldg_nc_u2(a.meta + (blk * 128 + tl) * 4 + 2 * (kt & 1)) : make_uint2(0x44444444u, 0x44444444u);
-                }
-                if (g >= ST) mbar_wait(&empty[s], uint32_t(((g / ST) - 1) & 1));
-                tc_fence_after();
-                if (!(a.exp & 64)) {
-#pragma unroll
-                    for (int mb = 0; mb < MB; ++mb)
-                        tmem_st_32x32b_x2(tE + uint32_t((s * MB + mb) * 2) + (uint32_t(32 * q) << 16), w[mb].x, w[mb].y);
-                    tmem_wait_st();
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&full[s]);
+            for (int mb = 0; mb < MB; ++mb) {
+                const bool in = g < total && (mb0 + mb) * 128 < sp24_m128(a.M) && !(a.exp & 8);
+                w[mb] = in ? ldg_nc_u2(a.meta + (((mb0 + mb) * a.KT + (kt >> 1)) * 128 + tl) * 4 + 2 * (kt & 1))
+                           : make_uint2(0x44444444u, 0x44444444u);
             }
+        };
+        uint2 cur[PF][MB], nxt[PF][MB];
+#pragma unroll
+        for (int j = 0; j < PF; ++j) load_stage(j, cur[j]);
+        for (int g0 = 0; g0 < total; g0 += PF) {
+#pragma unroll
+            for (int j = 0; j < PF; ++j) load_stage(g0 + PF + j, nxt[j]);
+#pragma unroll
+            for (int j = 0; j < PF; ++j) {
+                const int g = g0 + j;
+                if (g < total) {
+                    const int s = g % ST;
+                    if (g >= ST) mbar_wait(&empty[s], uint32_t(((g / ST) - 1) & 1));
+                    tc_fence_after();
+                    if (!(a.exp & 64)) {
+#pragma unroll
+                        for (int mb = 0; mb < MB; ++mb)
+                            tmem_st_32x32b_x2(tE + uint32_t((s * MB + mb) * 2) + (uint32_t(32 * q) << 16), cur[j][mb].x,
+                                              cur[j][mb].y);
+                        tmem_wait_st();
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&full[s]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < PF; ++j)
+#pragma unroll
+                for (int mb = 0; mb < MB; ++mb) cur[j][mb] = nxt[j][mb];
         }
     } else if (warp >= 8) {
         // ======================= epilogue =======================
@@ -370,6 +390,251 @@ spmm_sp24_kernel(const Sp24Args a, const __grid_constant__ CUtensorMap tmA, cons
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem, Cfg::kTmemCols);
+    }
+}
+
+// ---- 2-SM variant: cta_group::2 (a CTA pair on two SMs shares every MMA) -------------------------
+// The pair computes 256 rows x 256 tokens per tile with tcgen05.mma.sp.cta_group::2 (M = 256,
+// N = 256): each SM stages only ITS 128 rows of A and ITS 128 tokens of B (the MMA reads the two
+// halves of B from both SMs), so the per-SM shared-memory traffic per MMA drops from 4 KB + 16 KB to
+// 4 KB + 8 KB -- the sparse MMA is shared-memory bound in the 1-SM form.
+// Stages of 128 logical k: per CTA one A box [128 rows][64 stored k] (SWIZZLE_128B), two B boxes
+// [128 k][64 tokens] (SWIZZLE_128B) and the stage's metadata (128 lanes x 16 bytes, a 3-D TMA box of
+// the metadata image), all completing on the LEADER's (cluster rank 0) stage barrier; the leader's
+// MMA lane copies both CTAs' metadata into their TMEM (tcgen05.cp.cta_group::2 128x128b) and issues
+// 4 sparse MMAs; its commits arrive on both CTAs' empty / D-full barriers (multicast); both CTAs'
+// epilogue warps drain their own rows and arrive on the leader's D-empty barrier remotely.
+template <int ST>
+struct Sp24Cfg2 {
+    static constexpr int kBM = 256;                          // pair rows (128 per CTA)
+    static constexpr int kBN = 256;                          // pair tokens (128 per CTA's B half)
+    static constexpr int kAStage = 128 * 128;                // [128 rows][64 stored k] bf16 (SWIZZLE_128B)
+    static constexpr int kBStage = 128 * 128 * 2;            // [2 chunks][128 k][64 tokens] bf16 (SWIZZLE_128B)
+    static constexpr int kEStage = 2048;                     // [128 lanes][4 u32]
+    static constexpr int kStage = kAStage + kBStage + kEStage;
+    static constexpr int kHdr = 1024;
+    static constexpr int kStageOut = 8 * 32 * 32 * 4;
+    static constexpr size_t kSmem = size_t(kHdr) + size_t(ST) * kStage + kStageOut + 1024;
+    static constexpr int kDCols = 256;
+    static constexpr int kECols = ST * 4;
+    static constexpr int kThreads = 512;
+    static_assert(kDCols + kECols <= 512, "TMEM budget");
+    static_assert(kSmem <= 232448, "smem");
+};
+
+STEN_DEVICE_INLINE void tc_mma_sp_ss_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t e_tmem,
+                                         uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+        "tcgen05.mma.sp.cta_group::2.kind::f16 [%0], %1, %2, [%3], %4, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(e_tmem), "r"(idesc), "r"(acc)
+        : "memory");
+}
+STEN_DEVICE_INLINE void tc_cp_128x128b_2sm(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::2.128x128b [%0], %1;\n" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+STEN_DEVICE_INLINE void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+STEN_DEVICE_INLINE void tma_load_2d_2sm(void* smem_dst, const void* tmap, uint32_t bar_leader, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+        "[%2];\n" ::"r"(smem_u32(smem_dst)),
+        "l"(tmap), "r"(bar_leader), "r"(x), "r"(y)
+        : "memory");
+}
+STEN_DEVICE_INLINE void tma_load_3d_2sm(void* smem_dst, const void* tmap, uint32_t bar_leader, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+        "%5}], [%2];\n" ::"r"(smem_u32(smem_dst)),
+        "l"(tmap), "r"(bar_leader), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
+STEN_DEVICE_INLINE void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+STEN_DEVICE_INLINE void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAITC_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+template <typename TC, int ST>
+__global__ void __launch_bounds__(512, 1)
+spmm_sp24_2sm_kernel(const Sp24Args a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmE) {
+    using Cfg = Sp24Cfg2<ST>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);       // [ST] (leader) A + B + E of both CTAs
+    uint64_t* empty = full + ST;                               // [ST] (each) leader's MMA commit
+    uint64_t* dfull = empty + ST;                              // (each) leader's commit: tile accumulated
+    uint64_t* dempty = dfull + 1;                              // (leader) 16 epilogue warps: D read out
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 1);
+    auto sA = [&](int s) { return smem + Cfg::kHdr + size_t(s) * Cfg::kStage; };
+    auto sB = [&](int s) { return smem + Cfg::kHdr + size_t(s) * Cfg::kStage + Cfg::kAStage; };
+    auto sE = [&](int s) { return smem + Cfg::kHdr + size_t(s) * Cfg::kStage + Cfg::kAStage + Cfg::kBStage; };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();                   // 0 = leader
+    const int pair = int(blockIdx.x >> 1), npairs = int(gridDim.x >> 1);
+    const int nkt = int(a.KT);                                 // stages of 128 logical k
+    const int ntiles = a.row_tiles * a.col_tiles;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        mbar_init(dfull, 1);
+        mbar_init(dempty, 16);
+        fence_mbar_init();
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync_all();                                        // barriers of both CTAs initialised
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tD = tmem, tE = tmem + Cfg::kDCols;
+    const uint32_t full0 = map_cluster(smem_u32(full), 0);     // the leader's stage barriers
+    const uint32_t dempty0 = map_cluster(smem_u32(dempty), 0);
+
+    if (warp == 0) {
+        // ======================= TMA producer (both CTAs) =======================
+        if (lane == 0) {
+            asm volatile("griddepcontrol.wait;\n" ::: "memory");
+            int g = 0;
+            const int mrows = int(sp24_m128(a.M) / 128);
+            for (int t = pair; t < ntiles; t += npairs) {
+                const int64_t mblk = int64_t(t % a.row_tiles) * 2 + rank;        // this CTA's 128-row block
+                const int64_t n0 = int64_t(t / a.row_tiles) * Cfg::kBN + 128 * rank;
+                for (int kt = 0; kt < nkt; ++kt, ++g) {
+                    const int s = g % ST;
+                    if (g >= ST) mbar_wait(&empty[s], uint32_t(((g / ST) - 1) & 1));
+                    if (rank == 0) mbar_arrive_expect_tx(&full[s], (a.exp & 6) ? 0u : uint32_t(2 * Cfg::kStage));
+                    const uint32_t bar = full0 + uint32_t(s) * 8u;
+                    if (!(a.exp & 6)) {
+                        tma_load_2d_2sm(sA(s), &tmA, bar, kt * 64, int(mblk * 128));
+#pragma unroll
+                        for (int c = 0; c < 2; ++c)
+                            tma_load_2d_2sm(sB(s) + c * 16384, &tmB, bar, int(n0 + 64 * c), kt * 128);
+                        // metadata image block (mblk, kt); a block past M128 is clamped (its rows are padding)
+                        tma_load_3d_2sm(sE(s), &tmE, bar, 0, 0, int((mblk < mrows ? mblk : mrows - 1) * a.KT + kt));
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ======================= MMA issuer (leader only) =======================
+        if (rank == 0) {
+            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(256 >> 3) << 17) |
+                                   (uint32_t(256 >> 4) << 24) | (1u << 2) | (1u << 16);   // M 256, N 256, sparse, B MN-major
+            int g = 0, it = 0;
+            for (int t = pair; t < ntiles; t += npairs, ++it) {
+                if (it > 0) mbar_wait_cluster(dempty, uint32_t((it - 1) & 1));
+                tc_fence_after();
+                for (int kt = 0; kt < nkt; ++kt, ++g) {
+                    const int s = g % ST;
+                    mbar_wait_cluster(&full[s], uint32_t((g / ST) & 1));
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t a_base = smem_u32(sA(s)), b_base = smem_u32(sB(s));
+                        const uint32_t ecol = tE + uint32_t(s * 4);
+                        if (!(a.exp & 1)) {
+                            tc_cp_128x128b_2sm(ecol, tc_sdesc(smem_u32(sE(s)), 16, 128));
+                            const uint64_t adesc = tc_sdesc_sw128(a_base);
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                tc_mma_sp_ss_2sm(tD, adesc + uint64_t(kk * 2), tc_sdesc_mn_sw128(b_base + kk * 4096, 16384),
+                                                 ecol + uint32_t(kk & 2), idesc | uint32_t(kk & 1),
+                                                 (kt > 0 || kk > 0) ? 1u : 0u);
+                        }
+                        tc_commit_2sm_mc(&empty[s], uint16_t(0x3));
+                    }
+                    __syncwarp();
+                }
+                if (elect_one()) tc_commit_2sm_mc(dfull, uint16_t(0x3));
+                __syncwarp();
+            }
+        }
+    } else if (warp >= 8) {
+        // ======================= epilogue (both CTAs, own rows) =======================
+        const int q = warp & 3, h = (warp - 8) >> 2;
+        constexpr int HC = 128;                                        // columns per warp (of 256)
+        constexpr int ES = int(sizeof(TC));
+        unsigned char* stage_out = smem + Cfg::kHdr + size_t(ST) * Cfg::kStage + size_t(warp - 8) * 32 * 32 * 4;
+        int it = 0;
+        for (int t = pair; t < ntiles; t += npairs, ++it) {
+            const int64_t m0 = int64_t(t % a.row_tiles) * Cfg::kBM + 128 * rank;
+            const int64_t n0 = int64_t(t / a.row_tiles) * Cfg::kBN;
+            mbar_wait_cluster(dfull, uint32_t(it & 1));
+            tc_fence_after();
+            const int64_t row0 = m0 + 32 * q;
+#pragma unroll 1
+            for (int c0 = 0; c0 < HC; c0 += 32) {
+                uint32_t r[32];
+                if (!(a.exp & 32)) {
+                    tmem_ld_32x32b_x32(tD + (uint32_t(32 * q) << 16) + uint32_t(h * HC + c0), r);
+                    tmem_wait_ld();
+                }
+                if (c0 + 32 >= HC) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(dempty0);
+                }
+                const int64_t col0 = n0 + h * HC + c0;
+                if (row0 >= a.M || col0 >= a.N || (a.exp & 16)) continue;
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                __syncwarp();
+                unsigned char* srow = stage_out + size_t(lane) * 32 * ES;
+                constexpr int CH = 32 * ES / 16;
+#pragma unroll
+                for (int cc = 0; cc < CH; ++cc) {
+                    const int c = (cc + lane) % CH;
+                    uint4 u;
+                    if constexpr (ES == 4) {
+                        u = make_uint4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
+                    } else {
+                        uint32_t pk[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            pk[e] = uint32_t(f32_to_bf16_rne(__uint_as_float(r[8 * c + 2 * e]))) |
+                                    (uint32_t(f32_to_bf16_rne(__uint_as_float(r[8 * c + 2 * e + 1]))) << 16);
+                        u = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    }
+                    *reinterpret_cast<uint4*>(srow + c * 16) = u;
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(&tmC),
+                        "r"(int(col0)), "r"(int(row0)), "r"(smem_u32(stage_out))
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                }
+            }
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+        __syncwarp();
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();                                        // the peer's TMEM / smem stay alive until the pair is done
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512) : "memory");
     }
 }
 

@@ -59,7 +59,7 @@ def test_sp24_identity_is_densify(n, m, g):
 
 
 @pytest.mark.parametrize("n,m", [(2, 4), (1, 4), (2, 8), (1, 10)])
-@pytest.mark.parametrize("tile", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("tile", [1, 2, 3, 4, 5, 6])
 def test_sp24_integer_exact(n, m, tile):
     """P7: integer-valued bf16 inputs -> exact products and exact fp32 sums: bit-exact."""
     M, K, N = 300, m * 52, 333 + 3
