@@ -271,50 +271,30 @@ spmm_sp24_kernel(const Sp24Args a, const __grid_constant__ CUtensorMap tmA, cons
         // ======================= metadata writers =======================
         const int q = warp & 3;
         const int tl = 32 * q + lane;                                  // TMEM lane
-        // the metadata words of stage g (this CTA's g-th K-step over its tiles), prefetched PF stages
-        // ahead in registers: the L2 latency of one load per stage would otherwise pace the pipeline
-        constexpr int PF = 8;
-        const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
-        const int total = my_tiles * nkt;
-        auto load_stage = [&](int g, uint2 (&w)[MB]) {
-            const int t = int(blockIdx.x) + (g / nkt) * int(gridDim.x), kt = g % nkt;
+        int g = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int64_t mb0 = int64_t(t % a.row_tiles) * MB;
+            for (int kt = 0; kt < nkt; ++kt, ++g) {
+                const int s = g % ST;
+                uint2 w[MB];
 #pragma unroll
-            for (int mb = 0; mb < MB; ++mb) {
-                const bool in = g < total && (mb0 + mb) * 128 < sp24_m128(a.M) && !(a.exp & 8);
-                w[mb] = in ? ldg_nc_u2(a.meta + (((mb0 + mb) * a.KT + (kt >> 1)) * 128 + tl) * 4 + 2 * (kt & 1))
-                           : make_uint2(0x44444444u, 0x44444444u);
-            }
-        };
-        uint2 cur[PF][MB], nxt[PF][MB];
-#pragma unroll
-        for (int j = 0; j < PF; ++j) load_stage(j, cur[j]);
-        for (int g0 = 0; g0 < total; g0 += PF) {
-#pragma unroll
-            for (int j = 0; j < PF; ++j) load_stage(g0 + PF + j, nxt[j]);
-#pragma unroll
-            for (int j = 0; j < PF; ++j) {
-                const int g = g0 + j;
-                if (g < total) {
-                    const int s = g % ST;
-                    if (g >= ST) mbar_wait(&empty[s], uint32_t(((g / ST) - 1) & 1));
-                    tc_fence_after();
-                    if (!(a.exp & 64)) {
-#pragma unroll
-                        for (int mb = 0; mb < MB; ++mb)
-                            tmem_st_32x32b_x2(tE + uint32_t((s * MB + mb) * 2) + (uint32_t(32 * q) << 16), cur[j][mb].x,
-                                              cur[j][mb].y);
-                        tmem_wait_st();
-                    }
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&full[s]);
+                for (int mb = 0; mb < MB; ++mb) {
+                    const int64_t blk = (mb0 + mb) * a.KT + (kt >> 1);
+                    const bool in = (mb0 + mb) * 128 < sp24_m128(a.M) && !(a.exp & 8);
+                    w[mb] = in ? ldg_nc_u2(a.meta + (blk * 128 + tl) * 4 + 2 * (kt & 1)) : make_uint2(0x44444444u, 0x44444444u);
                 }
+                if (g >= ST) mbar_wait(&empty[s], uint32_t(((g / ST) - 1) & 1));
+                tc_fence_after();
+                if (!(a.exp & 64)) {
+#pragma unroll
+                    for (int mb = 0; mb < MB; ++mb)
+                        tmem_st_32x32b_x2(tE + uint32_t((s * MB + mb) * 2) + (uint32_t(32 * q) << 16), w[mb].x, w[mb].y);
+                    tmem_wait_st();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[s]);
             }
-#pragma unroll
-            for (int j = 0; j < PF; ++j)
-#pragma unroll
-                for (int mb = 0; mb < MB; ++mb) cur[j][mb] = nxt[j][mb];
         }
     } else if (warp >= 8) {
         // ======================= epilogue =======================
