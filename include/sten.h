@@ -394,6 +394,16 @@ sten_status sten_spmm_sp24(const void* v24, const uint32_t* meta, int64_t M, int
                            const void* B, int64_t ldb, int64_t N,
                            void* C, int64_t ldc, sten_dtype c_dt, int32_t tile, void* stream);
 
+/* sten_spmm_sp24 with the fused epilogue of NEXT-3 (a transformer linear on the tensor cores):
+ *   C = act(densify(values, idx) x B + bias[row]) + R[row][col]
+ * bias [M] fp32 or NULL, act 0 none / 1 GELU (erf) / 2 ReLU, R [M][ldr] of c_dt or NULL (must not
+ * alias C; ldr >= N).  Applied to the fp32 accumulators after the TMEM read, before the store. */
+sten_status sten_spmm_sp24_epilogue(const void* v24, const uint32_t* meta, int64_t M, int64_t K,
+                                    const void* B, int64_t ldb, int64_t N,
+                                    void* C, int64_t ldc, sten_dtype c_dt,
+                                    const float* bias, int32_t act, const void* residual, int64_t ldr,
+                                    int32_t tile, void* stream);
+
 const char* sten_status_string(sten_status s);
 const char* sten_algo_name(int32_t algo);
 /* Number of kernel launches the last call of each entry point enqueues is

@@ -199,6 +199,14 @@ sten_status sten_sp24_pack(sten_nmg f, sten_dtype dt, const void* values, const 
 
 sten_status sten_spmm_sp24(const void* v24, const uint32_t* meta, int64_t M, int64_t K, const void* B, int64_t ldb,
                            int64_t N, void* C, int64_t ldc, sten_dtype c_dt, int32_t tile, void* stream) {
+    return sten_spmm_sp24_epilogue(v24, meta, M, K, B, ldb, N, C, ldc, c_dt, nullptr, 0, nullptr, 0, tile, stream);
+}
+
+sten_status sten_spmm_sp24_epilogue(const void* v24, const uint32_t* meta, int64_t M, int64_t K, const void* B,
+                                    int64_t ldb, int64_t N, void* C, int64_t ldc, sten_dtype c_dt, const float* bias,
+                                    int32_t act, const void* residual, int64_t ldr, int32_t tile, void* stream) {
+    if (act < 0 || act > 2) return STEN_ERR_INVALID_ARG;
+    if (residual && (ldr < N || residual == C)) return residual == C ? STEN_ERR_INVALID_ARG : STEN_ERR_SHAPE;
     if (M < 0 || K < 0 || N < 0 || ldb < N || ldc < N) return STEN_ERR_SHAPE;
     if (c_dt != STEN_F32 && c_dt != STEN_BF16) return STEN_ERR_INVALID_ARG;
     if ((M * K > 0 && (!v24 || !meta)) || (K * N > 0 && !B) || (M * N > 0 && !C)) return STEN_ERR_INVALID_ARG;
@@ -225,6 +233,10 @@ sten_status sten_spmm_sp24(const void* v24, const uint32_t* meta, int64_t M, int
     a.Kc = sp24_k128(K) / 2;
     const size_t sc = c_dt == STEN_F32 ? 4 : 2;
     a.c_vec = al16(C) && (size_t(ldc) * sc) % 16 == 0;
+    a.bias = bias;
+    a.act = act;
+    a.residual = residual;
+    a.ldr = ldr;
     if (const char* e = getenv("STEN_SP24_EXP")) a.exp = atoi(e);     // debug timing experiments only
     return c_dt == STEN_F32 ? launch_sp24_tile<float>(a, tile, st) : launch_sp24_tile<bf16_t>(a, tile, st);
 }

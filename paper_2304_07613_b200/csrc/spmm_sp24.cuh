@@ -99,10 +99,32 @@ struct Sp24Args {
     int nkt;               // K-steps of 64 logical k per tile (stages)
     int row_tiles, col_tiles;
     bool c_vec;
+    // fused epilogue (NEXT-3 on the tensor-core path): C = act(A.B + bias[row]) + residual[row][col]
+    const float* bias;     // [M] fp32 or NULL
+    int act;               // 0 none, 1 GELU (erf form), 2 ReLU
+    const void* residual;  // [M][ldr] of the C dtype or NULL
+    int64_t ldr;
     int exp;               // debug experiments (STEN_SP24_EXP, timing only): 1 no MMA, 2 no B loads,
                            // 4 no A loads, 8 no metadata, 16 no epilogue stores, 32 no TMEM
                            // drain, 64 no metadata TMEM stores
 };
+
+// the fused epilogue on 32 consecutive tokens [col, col + 32) of one row (fp32 accumulators as bits)
+template <typename TC>
+STEN_DEVICE_INLINE void sp24_epilogue(const Sp24Args& a, int64_t row, int64_t col, uint32_t (&r)[32]) {
+    if (!a.bias && !a.act && !a.residual) return;
+    if (row >= a.M) return;
+    const float b = a.bias ? a.bias[row] : 0.0f;
+    const TC* R = a.residual ? static_cast<const TC*>(a.residual) + row * a.ldr : nullptr;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        float x = __uint_as_float(r[j]) + b;
+        if (a.act == 1) x = 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+        else if (a.act == 2) x = fmaxf(x, 0.0f);
+        if (R && col + j < a.N) x = __fadd_rn(x, to_f32(R[col + j]));
+        r[j] = __float_as_uint(x);
+    }
+}
 
 STEN_DEVICE_INLINE void tc_mma_sp_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t e_tmem,
                                      uint32_t idesc, uint32_t acc) {
@@ -327,6 +349,7 @@ spmm_sp24_kernel(const Sp24Args a, const __grid_constant__ CUtensorMap tmA, cons
                     }
                     const int64_t col0 = n0 + h * HC + c0;
                     if (row0 >= a.M || col0 >= a.N || (a.exp & 16)) continue;
+                    sp24_epilogue<TC>(a, row0 + lane, col0, r);
                     // the previous TMA store of this warp has finished reading the staging tile
                     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
                     __syncwarp();
@@ -575,6 +598,7 @@ spmm_sp24_2sm_kernel(const Sp24Args a, const __grid_constant__ CUtensorMap tmA, 
                 }
                 const int64_t col0 = n0 + h * HC + c0;
                 if (row0 >= a.M || col0 >= a.N || (a.exp & 16)) continue;
+                sp24_epilogue<TC>(a, row0 + lane, col0, r);
                 if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
                 __syncwarp();
                 unsigned char* srow = stage_out + size_t(lane) * 32 * ES;

@@ -11,7 +11,9 @@ C = y^T), so the four linears of a layer chain without transpo
     y^T   = LN(W2 . f^T + b2 + h^T)                             (SpMM, bias + residual in the epilogue)
 
 Attention (SDPA) and LayerNorm run as torch ops (layout copies around SDPA are device-memory
-plumbing); every linear is ONE launch of the library's SIMT SpMM with its epilogue fused.  The dense
+plumbing); every linear is ONE launch of the library's SpMM with its epilogue fused: the SIMT kernel
+(fp32), or for bf16 with a 2:4-compatible format the 2:4 structured-sparse tensor-core kernel (K6,
+weights packed once at load).  The dense
 reference (`DenseBertLayer`) is the same layer with cuBLAS GEMMs on densify(W) -- the GPU analogue
 of the paper's "vs dense PyTorch" comparison.
 """
@@ -62,13 +64,19 @@ def random_layer_weights(seed: int, device) -> dict:
 class SparseBertLayer:
     """One encoder layer with its four linears in grouped n:m form (sparsified once, at load)."""
 
-    def __init__(self, wts: dict, n: int, m: int, g: int, dtype=torch.float32):
+    def __init__(self, wts: dict, n: int, m: int, g: int, dtype=torch.float32, backend: str | None = None):
         self.fmt = (n, m, g)
         self.dtype = dtype
+        # bf16 with a 2:4-compatible format -> the 2:4 structured-sparse tensor cores (K6, fused epilogue);
+        # otherwise the SIMT SpMM with its fused epilogue
+        self.backend = backend or ("sp24" if dtype == torch.bfloat16 and sten.sp24_compatible(n, m) else "simt")
         self.lin = {}
+        self.packed = {}
         for name in ("qkv", "o", "w1", "w2"):
             W = wts[name].to(dtype).contiguous()
             self.lin[name] = sten.sparsify_grouped_nm(W, n, m, g)
+            if self.backend == "sp24":
+                self.packed[name] = sten.sp24_pack(*self.lin[name], n, m, g, W.shape[1])
         self.bias = {k: wts[k].float().contiguous() for k in ("bqkv", "bo", "b1", "b2")}
         self.ln = {k: wts[k].to(dtype) for k in ("ln1_g", "ln1_b", "ln2_g", "ln2_b")}
 
@@ -80,15 +88,21 @@ class SparseBertLayer:
             out[name] = sten.densify(v, i, n, m, g, i.shape[1] * m)
         return out
 
-    def __call__(self, xT: torch.Tensor, batch: int, seq: int) -> torch.Tensor:
+    def _linear(self, name: str, B: torch.Tensor, bias, act: int = 0, residual=None) -> torch.Tensor:
         n, m, g = self.fmt
-        ep = sten.spmm_grouped_nm_epilogue
-        qkv = ep(*self.lin["qkv"], xT, n, m, g, bias=self.bias["bqkv"])
+        if self.backend == "sp24":
+            v24, meta = self.packed[name]
+            return sten.spmm_sp24_epilogue(v24, meta, self.lin[name][0].shape[0], B.shape[0], B, bias=bias, act=act,
+                                           residual=residual, out_dtype=self.dtype)
+        return sten.spmm_grouped_nm_epilogue(*self.lin[name], B, n, m, g, bias=bias, act=act, residual=residual)
+
+    def __call__(self, xT: torch.Tensor, batch: int, seq: int) -> torch.Tensor:
+        qkv = self._linear("qkv", xT, self.bias["bqkv"])
         aT = attention_fm(qkv, batch, seq)
-        h = ep(*self.lin["o"], aT, n, m, g, bias=self.bias["bo"], residual=xT)
+        h = self._linear("o", aT, self.bias["bo"], residual=xT)
         h = layer_norm_fm(h, self.ln["ln1_g"], self.ln["ln1_b"]).contiguous()
-        f = ep(*self.lin["w1"], h, n, m, g, bias=self.bias["b1"], act=sten.ACT_GELU)
-        y = ep(*self.lin["w2"], f, n, m, g, bias=self.bias["b2"], residual=h)
+        f = self._linear("w1", h, self.bias["b1"], act=sten.ACT_GELU)
+        y = self._linear("w2", f, self.bias["b2"], residual=h)
         return layer_norm_fm(y, self.ln["ln2_g"], self.ln["ln2_b"]).contiguous()
 
 

@@ -109,6 +109,8 @@ SIGNATURES = {
     "sten_sp24_pack": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "sten_spmm_sp24": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, ctypes.c_int,
                                       ctypes.c_int32, _vp]),
+    "sten_spmm_sp24_epilogue": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, ctypes.c_int,
+                                               _vp, ctypes.c_int32, _vp, _i64, ctypes.c_int32, _vp]),
     "sten_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "sten_algo_name": (ctypes.c_char_p, [ctypes.c_int32]),
     "sten_spmm_launch_count": (ctypes.c_int32, [ctypes.POINTER(sten_spmm_plan)]),
@@ -586,4 +588,26 @@ def spmm_sp24(v24: torch.Tensor, meta: torch.Tensor, M: int, K: int, B: torch.Te
         out = torch.empty((M, N), dtype=out_dtype or torch.bfloat16, device=B.device)
     _check(load().sten_spmm_sp24(v24.data_ptr(), meta.data_ptr(), M, K, B.data_ptr(), _ld(B), N, out.data_ptr(),
                                  _ld(out), _dt(out), int(tile), _stream(stream)), "sten_spmm_sp24")
+    return out
+
+
+def spmm_sp24_epilogue(v24: torch.Tensor, meta: torch.Tensor, M: int, K: int, B: torch.Tensor,
+                       bias: torch.Tensor | None = None, act: int = 0, residual: torch.Tensor | None = None,
+                       out: torch.Tensor | None = None, out_dtype=None, tile: int = 0, stream=None) -> torch.Tensor:
+    """C = act(densify @ B + bias[:, None]) + residual on the 2:4 sparse tensor cores (sten_spmm_sp24_epilogue)."""
+    _cuda(B, "B")
+    if B.dtype != torch.bfloat16:
+        raise TypeError("sten_spmm_sp24 takes bf16 B")
+    N = B.shape[1]
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype or torch.bfloat16, device=B.device)
+    if bias is not None and (bias.dtype != torch.float32 or bias.numel() != M or not bias.is_contiguous()):
+        raise ValueError("bias must be a contiguous float32 vector of length M")
+    if residual is not None and (residual.dtype != out.dtype or tuple(residual.shape) != (M, N)):
+        raise ValueError("residual must be [M][N] in the output dtype")
+    _check(load().sten_spmm_sp24_epilogue(
+        v24.data_ptr(), meta.data_ptr(), M, K, B.data_ptr(), _ld(B), N, out.data_ptr(), _ld(out), _dt(out),
+        bias.data_ptr() if bias is not None else None, int(act),
+        residual.data_ptr() if residual is not None else None, _ld(residual) if residual is not None else 0,
+        int(tile), _stream(stream)), "sten_spmm_sp24_epilogue")
     return out

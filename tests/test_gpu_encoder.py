@@ -96,3 +96,40 @@ def test_encoder_graph_replay_equals_eager():
     out = enc.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, eager)
+
+
+@pytest.mark.parametrize("act", [0, 1])
+@pytest.mark.parametrize("tile", [1, 6])
+def test_sp24_epilogue(act, tile):
+    """The fused bias / GELU / residual epilogue of K6 against the oracle (bf16 in, fp32 out)."""
+    n, m, g, M, K, N = 2, 4, 4, 384, 2048, 300
+    W = synthetic.weights(M, K, seed=51, dtype="bf16")
+    B = synthetic.activations(K, N, seed=52, dtype="bf16")
+    R = synthetic.activations(M, N, seed=53)
+    bias = (np.random.default_rng(54).standard_normal(M) * 0.1).astype(np.float32)
+    v, i = sten.sparsify_grouped_nm(dev(W, "bf16"), n, m, g)
+    v24, meta = sten.sp24_pack(v, i, n, m, g, K)
+    C = sten.spmm_sp24_epilogue(v24, meta, M, K, dev(B, "bf16"), bias=torch.from_numpy(bias).cuda(), act=act,
+                                residual=dev(R, "f32"), out_dtype=torch.float32, tile=tile)
+    torch.cuda.synchronize()
+    v_ref, i_ref = oracle.sparsify(W, n, m, g)
+    C_ref, Bound = oracle.spmm(v_ref, i_ref, B, n, m, g)
+    ref = oracle.bias_act(C_ref, bias, act) + R.astype(np.float64)
+    err = np.abs(C.cpu().numpy().astype(np.float64) - ref)
+    assert (err <= 1.13 * 1e-5 * Bound + 1e-5 * (np.abs(ref) + 1)).all()
+
+
+def test_encoder_layer_bf16_sp24_vs_fp64_reference():
+    """The bf16 encoder layer on the 2:4 sparse tensor cores vs the fp64 reference (bf16 tolerance)."""
+    batch, seq, n, m, g = 2, 32, 2, 4, 4
+    wts = encoder.random_layer_weights(8, "cpu")
+    layer = encoder.SparseBertLayer({k: v.cuda() for k, v in wts.items()}, n, m, g, dtype=torch.bfloat16)
+    assert layer.backend == "sp24"
+    x = synthetic.activations(768, batch * seq, seed=10, dtype="bf16")
+    y = layer(torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda(), batch, seq)
+    torch.cuda.synchronize()
+    wb = {k: synthetic.bf16_bits_to_f32(synthetic.f32_to_bf16_bits(v.numpy())) if k in ("qkv", "o", "w1", "w2")
+          else v.numpy() for k, v in wts.items()}
+    ref = _reference_layer(wb, synthetic.bf16_bits_to_f32(x), batch, seq, n, m, g)
+    err = float(np.max(np.abs(y.float().cpu().numpy().astype(np.float64) - ref)))
+    assert err <= 0.15, err                     # bf16 activations between layers; post-LN values are O(1)
