@@ -575,8 +575,8 @@ def bench_sten(args, rank, world, local_rank):
                 "frac": round(achieved / peak, 4), "traffic": measured_traffic(cfg, dtype, mode),
                 "algorithmic_bytes_per_launch": round(sum(spmm_bytes(c) for c in cases) / len(cases), 1),
                 "peak_source": peaks["fp32_source"],
-                "kernel": ("spmm_simt_batched_kernel (one grouped split-K launch of the step's %d SpMMs, CUDA-core "
-                           "FFMA2)" % len(cases)) if mode == "grouped" else "spmm_simt_kernel (CUDA-core FFMA)"}
+                "kernel": ("spmm_simt_batched(2)_kernel (one grouped split-K launch of the step's %d SpMMs, "
+                           "CUDA-core FFMA2)" % len(cases)) if mode == "grouped" else "spmm_simt_kernel (CUDA-core FFMA)"}
     else:
         t_roof = sum(max(nz_flops(c) / (peaks["bf16_tflops"] * 1e12), spmm_bytes(c) / (peaks["hbm_gbs"] * 1e9))
                      for c in cases) * args.steps
@@ -886,7 +886,8 @@ def per_kernel_b2b(cases, data, dtype, device, l2, steps, sp24=False):
                    "spmm_us_in_step / sparsify_us_in_step = the event brackets inside the single-stream step"}
 
 
-GROUPED_TILE = 2        # 16-warp SIMT tile (BM 120 x BN 256): fastest grouped step (tools/grouped_probe.py)
+GROUPED_TILE = 2        # the 16-warp 120 x 256 SIMT tile for every problem: fastest grouped step; the per-problem
+                        # mix (tile 0: tile 3 for 1:10) measured equal (tools/grouped_split_probe.py)
 
 
 def grouped_b2b(cases, sets, grouped):

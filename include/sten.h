@@ -236,8 +236,10 @@ sten_status sten_spmm_grouped_nm_batched(int32_t count, const sten_spmm_problem*
  * workspace: caller-allocated, >= sten_spmm_batched_workspace_size bytes, 16-byte aligned; it
  * starts with one counter per split tile that MUST be zero before the first call (memset the
  * buffer once after allocating it); every call leaves them at zero.  Calls sharing a workspace
- * must be stream-ordered.  Other arguments and errors as sten_spmm_grouped_nm_batched; a workspace
- * smaller than needed -> STEN_ERR_SHAPE, NULL while needed -> STEN_ERR_INVALID_ARG. */
+ * must be stream-ordered.  tile: 1 / 2 / 3 = that SIMT tile for every problem; 0 = per problem (the
+ * 240-row x 128-token tile 3, whose K-slabs are 3x longer, for m >= 8 n; the 120 x 256 tile 2
+ * otherwise -- both in ONE launch).  Other arguments and errors as sten_spmm_grouped_nm_batched; a
+ * workspace smaller than needed -> STEN_ERR_SHAPE, NULL while needed -> STEN_ERR_INVALID_ARG. */
 sten_status sten_spmm_grouped_nm_batched_ex(int32_t count, const sten_spmm_problem* problems,
                                             const int32_t* splits, int32_t tile,
                                             void* workspace, int64_t workspace_bytes, void* stream);

@@ -691,6 +691,7 @@ struct SpmmBatch {
     CUtensorMap tmV[kMaxBatch];
     int tile0[kMaxBatch + 1];    // first CTA of each problem; tile0[count] = grid size
     int ntx[kMaxBatch];          // N tiles of each problem
+    int var[kMaxBatch];          // mixed launch: which of the two tile variants serves the problem
     int count;
 };
 // CTA b -> problem p, part z = unit % S (the S parts of a tile are adjacent CTAs), tile = unit / S
@@ -706,6 +707,26 @@ spmm_simt_batched_kernel(const __grid_constant__ SpmmBatch bt) {
     const int t = u / S;
     spmm_simt_body<TAB, TC, RG, TN, SUB, WARPS, MINB>(bt.a[p], &bt.tmB[p], &bt.tmV[p], t % bt.ntx[p],
                                                        t / bt.ntx[p], u - t * S);
+}
+
+// Mixed grouped launch: two tile variants with the same warp count in ONE launch (e.g. the 256-token
+// tile for 2:4 / 1:4 and the 240-row tile, with 3x longer K-slabs, for 1:10); bt.var[p] selects the
+// body of problem p.  Shared memory = the larger layout; registers = the larger variant.
+template <typename TAB, typename TC, int RG, int TNA, int SUBA, int TNB, int SUBB, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+spmm_simt_batched2_kernel(const __grid_constant__ SpmmBatch bt) {
+    const int b = int(blockIdx.x);
+    int p = 0;
+    while (p + 1 < bt.count && b >= bt.tile0[p + 1]) ++p;
+    const int u = b - bt.tile0[p];
+    const int S = bt.a[p].split;
+    const int t = u / S;
+    if (bt.var[p] == 0)
+        spmm_simt_body<TAB, TC, RG, TNA, SUBA, WARPS, 1>(bt.a[p], &bt.tmB[p], &bt.tmV[p], t % bt.ntx[p], t / bt.ntx[p],
+                                                         u - t * S);
+    else
+        spmm_simt_body<TAB, TC, RG, TNB, SUBB, WARPS, 1>(bt.a[p], &bt.tmB[p], &bt.tmV[p], t % bt.ntx[p], t / bt.ntx[p],
+                                                         u - t * S);
 }
 
 }  // namespace sten

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -294,12 +295,58 @@ sten_status launch_simt_batch_cfg(SpmmArgs* as, int count, cudaStream_t st) {
     return last_cuda();
 }
 
+// mixed grouped launch: tile 2 (variant 0) and tile 3 (variant 1) problems in one launch
+template <int RG>
+sten_status launch_simt_batch_mixed(SpmmArgs* as, const int* tiles_of, int count, cudaStream_t st) {
+    constexpr int SUB8 = 8 / RG;
+    using CfgA = SimtCfg<float, RG, 8, SUB8, 16>;
+    using CfgB = SimtCfg<float, RG, 4, 2 * SUB8, 16>;
+    SpmmBatch bt;
+    memset(&bt, 0, sizeof(bt));
+    size_t smem_max = 0;
+    int tiles = 0;
+    for (int p = 0; p < count; ++p) {
+        size_t sm = 0;
+        const bool vb = tiles_of[p] == 3;
+        sten_status ps = vb ? prep_simt<float, RG, 4, 2 * SUB8, 16>(as[p], &bt.tmB[p], &bt.tmV[p], &sm)
+                            : prep_simt<float, RG, 8, SUB8, 16>(as[p], &bt.tmB[p], &bt.tmV[p], &sm);
+        if (ps) return ps;
+        bt.a[p] = as[p];
+        const int bm = vb ? CfgB::kBM : CfgA::kBM, bn = vb ? CfgB::kBN : CfgA::kBN;
+        const int ntx = int((as[p].N + bn - 1) / bn), nty = int((as[p].M + bm - 1) / bm);
+        bt.tile0[p] = tiles;
+        bt.ntx[p] = ntx;
+        bt.var[p] = vb ? 1 : 0;
+        tiles += ntx * nty * as[p].split;
+        smem_max = std::max(smem_max, sm);
+    }
+    bt.tile0[count] = tiles;
+    bt.count = count;
+    if (tiles == 0) return STEN_OK;
+    auto kern = spmm_simt_batched2_kernel<float, float, RG, 8, SUB8, 4, 2 * SUB8, 16>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max)) != cudaSuccess)
+        return STEN_ERR_CUDA;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(tiles));
+    cfg.blockDim = dim3(16 * 32);
+    cfg.dynamicSmemBytes = smem_max;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, bt) != cudaSuccess) return STEN_ERR_CUDA;
+    return last_cuda();
+}
+
 template <int RG>
 sten_status launch_simt_batch_rg(SpmmArgs* as, int count, int tile, cudaStream_t st) {
     constexpr int SUB8 = 8 / RG;
     switch (tile) {
         case 1: return launch_simt_batch_cfg<RG, 8, SUB8, 8>(as, count, st);
         case 2: return launch_simt_batch_cfg<RG, 8, SUB8, 16>(as, count, st);
+        case 3: return launch_simt_batch_cfg<RG, 4, 2 * SUB8, 16>(as, count, st);
     }
     return STEN_ERR_UNSUPPORTED;
 }
@@ -662,19 +709,25 @@ namespace {
 
 // BM / BN of the batched tiles (tile 1: 8 warps, tile 2: 16 warps; TN = 8, RG * SUB = 8 rows per warp)
 inline void batch_tile_dims(int tile, int* bm, int* bn) {
-    *bm = (tile == 2 ? 15 : 7) * 8;
-    *bn = 256;
+    *bm = kSimtTiles[tile].bm;
+    *bn = 32 * kSimtTiles[tile].tn;
 }
 
 // Validate the problems and fill their kernel arguments; splits[p] (0 = auto) -> a.split.
 // Auto: every problem's K is cut into parts of about the same number of FMAs, so that the units of
 // all problems together give ~3 units per resident CTA slot (the block scheduler balances them).
+// the tile of problem p in a grouped launch: the caller's, or (tile 0) per problem: the 240-row,
+// 128-token tile (3x longer K-slabs) for m >= 8 n sparsity, the 120 x 256 tile otherwise
+inline int batch_tile_of(const sten_spmm_problem& q, int tile) {
+    if (tile) return tile;
+    return q.f.m >= 8 * q.f.n ? 3 : 2;
+}
+
 sten_status batch_setup(int32_t count, const sten_spmm_problem* probs, const int32_t* splits, int32_t tile,
                         SpmmArgs* as, int64_t* ws_floats, int64_t* ctr_words) {
     if (count < 1 || count > kMaxBatch || !probs) return STEN_ERR_INVALID_ARG;
-    if (tile != 1 && tile != 2) return STEN_ERR_UNSUPPORTED;
+    if (tile != 0 && tile != 1 && tile != 2 && tile != 3) return STEN_ERR_UNSUPPORTED;
     int bm, bn;
-    batch_tile_dims(tile, &bm, &bn);
     const int rg = simt_rows_per_warp(probs[0].f.g);
     double tot = 0;
     for (int p = 0; p < count; ++p) {
@@ -700,17 +753,22 @@ sten_status batch_setup(int32_t count, const sten_spmm_problem* probs, const int
         a.c_vec = aligned16(q.C) && (q.ldc * 4) % 16 == 0;
         a.v_async = (a.Kp % 4 == 0) && ((reinterpret_cast<uintptr_t>(q.values) & 15u) == 0);
         a.idx_bytes = (q.M / f.g) * a.KB * f.n;
-        a.kbs = simt_slab_blocks(f, STEN_F32, tile);
+        const int pt = batch_tile_of(q, tile);
+        batch_tile_dims(pt, &bm, &bn);
+        a.kbs = simt_slab_blocks(f, STEN_F32, pt);
         a.split = 1;
         a.kb_per_split = a.KB;
         const double tiles = double((q.N + bn - 1) / bn) * double((q.M + bm - 1) / bm);
         tot += tiles * double(bm) * bn * double(a.Kp);
     }
-    const double slots = double(kNumSMs) * (tile == 2 ? 1 : 2);
-    const double unit = tot / (3.0 * slots);                       // target FMAs per unit
+    const double slots = double(kNumSMs) * kSimtTiles[batch_tile_of(probs[0], tile)].per_sm;
+    double upc = 1.5;                                              // units per resident CTA slot (measured)
+    if (const char* e = getenv("STEN_GROUP_UNITS")) upc = atof(e);  // (tuning experiments only)
+    const double unit = tot / (upc * slots);                       // target FMAs per unit
     int64_t wsf = 0, ctrw = 0;
     for (int p = 0; p < count; ++p) {
         SpmmArgs& a = as[p];
+        batch_tile_dims(batch_tile_of(probs[p], tile), &bm, &bn);
         const int64_t slabs = (a.KB + a.kbs - 1) / a.kbs;
         int S = splits ? splits[p] : 0;
         if (S == 0) {
@@ -737,7 +795,6 @@ extern "C" {
 sten_status sten_spmm_batched_workspace_size(int32_t count, const sten_spmm_problem* probs, const int32_t* splits,
                                              int32_t tile, int64_t* bytes) {
     if (!bytes) return STEN_ERR_INVALID_ARG;
-    if (tile == 0) tile = 1;
     SpmmArgs as[kMaxBatch];
     int64_t wsf = 0, ctrw = 0;
     sten_status s = batch_setup(count, probs, splits, tile, as, &wsf, &ctrw);
@@ -748,7 +805,6 @@ sten_status sten_spmm_batched_workspace_size(int32_t count, const sten_spmm_prob
 
 sten_status sten_spmm_grouped_nm_batched_ex(int32_t count, const sten_spmm_problem* probs, const int32_t* splits,
                                             int32_t tile, void* workspace, int64_t workspace_bytes, void* stream) {
-    if (tile == 0) tile = 1;
     SpmmArgs as[kMaxBatch];
     int64_t wsf = 0, ctrw = 0;
     sten_status s = batch_setup(count, probs, splits, tile, as, &wsf, &ctrw);
@@ -760,9 +816,9 @@ sten_status sten_spmm_grouped_nm_batched_ex(int32_t count, const sten_spmm_probl
         unsigned* ctr = static_cast<unsigned*>(workspace);
         float* ws = reinterpret_cast<float*>(static_cast<char*>(workspace) + ctrw * 4);
         int bm, bn;
-        batch_tile_dims(tile, &bm, &bn);
         for (int p = 0; p < count; ++p) {
             SpmmArgs& a = as[p];
+            batch_tile_dims(batch_tile_of(probs[p], tile), &bm, &bn);
             if (a.split <= 1 || a.M == 0 || a.N == 0) continue;
             const int64_t tiles = ((a.N + bn - 1) / bn) * ((a.M + bm - 1) / bm);
             a.ws = ws;
@@ -777,17 +833,31 @@ sten_status sten_spmm_grouped_nm_batched_ex(int32_t count, const sten_spmm_probl
     std::stable_sort(order, order + count,
                      [&](int x, int y) { return as[x].Kp / as[x].split > as[y].Kp / as[y].split; });
     SpmmArgs sorted[kMaxBatch];
+    int tiles_of[kMaxBatch];
     int live = 0;
     for (int p = 0; p < count; ++p)
-        if (as[order[p]].M > 0 && as[order[p]].N > 0) sorted[live++] = as[order[p]];
+        if (as[order[p]].M > 0 && as[order[p]].N > 0) {
+            tiles_of[live] = batch_tile_of(probs[order[p]], tile);
+            sorted[live++] = as[order[p]];
+        }
     if (live == 0) return STEN_OK;
     const int rg = simt_rows_per_warp(probs[0].f.g);
     cudaStream_t st = as_stream(stream);
+    bool mixed = false;
+    for (int p = 1; p < live; ++p) mixed |= tiles_of[p] != tiles_of[0];
+    if (mixed) {
+        switch (rg) {
+            case 8: return launch_simt_batch_mixed<8>(sorted, tiles_of, live, st);
+            case 4: return launch_simt_batch_mixed<4>(sorted, tiles_of, live, st);
+            case 2: return launch_simt_batch_mixed<2>(sorted, tiles_of, live, st);
+            default: return launch_simt_batch_mixed<1>(sorted, tiles_of, live, st);
+        }
+    }
     switch (rg) {
-        case 8: return launch_simt_batch_rg<8>(sorted, live, tile, st);
-        case 4: return launch_simt_batch_rg<4>(sorted, live, tile, st);
-        case 2: return launch_simt_batch_rg<2>(sorted, live, tile, st);
-        default: return launch_simt_batch_rg<1>(sorted, live, tile, st);
+        case 8: return launch_simt_batch_rg<8>(sorted, live, tiles_of[0], st);
+        case 4: return launch_simt_batch_rg<4>(sorted, live, tiles_of[0], st);
+        case 2: return launch_simt_batch_rg<2>(sorted, live, tiles_of[0], st);
+        default: return launch_simt_batch_rg<1>(sorted, live, tiles_of[0], st);
     }
 }
 
@@ -797,6 +867,8 @@ sten_status sten_spmm_grouped_nm_batched(int32_t count, const sten_spmm_problem*
     int32_t ones[kMaxBatch];
     for (int p = 0; p < kMaxBatch; ++p) ones[p] = 1;
     if (count < 1 || count > kMaxBatch) return STEN_ERR_INVALID_ARG;
+    if (tile == 0) tile = 1;
+    if (tile != 1 && tile != 2) return STEN_ERR_UNSUPPORTED;
     return sten_spmm_grouped_nm_batched_ex(count, probs, ones, tile, nullptr, 0, stream);
 }
 

@@ -549,7 +549,7 @@ def test_spmm_batched_equals_single_launches(tile):
         assert rel_err(C, C_ref, Bound) <= 1e-5
 
 
-@pytest.mark.parametrize("tile", [1, 2])
+@pytest.mark.parametrize("tile", [0, 1, 2, 3])
 @pytest.mark.parametrize("splits", [None, [3, 2, 1, 5]])
 def test_spmm_batched_split_k_equals_cluster_split(tile, splits):
     """The grouped launch with per-problem split-K through the workspace equals, bit for bit, the
@@ -575,7 +575,8 @@ def test_spmm_batched_split_k_equals_cluster_split(tile, splits):
         for k, ((v, i, Bd, n, m, g_, C), (C_ref, Bound)) in enumerate(zip(probs, refs)):
             assert rel_err(C, C_ref, Bound) <= 1e-5
             if splits is not None:
-                S = sten.spmm_grouped_nm(v, i, Bd, n, m, g, plan=sten.make_plan(sten.ALGO_SIMT, splits[k], tile))
+                t = tile if tile else (3 if m >= 8 * n else 2)
+                S = sten.spmm_grouped_nm(v, i, Bd, n, m, g, plan=sten.make_plan(sten.ALGO_SIMT, splits[k], t))
                 torch.cuda.synchronize()
                 assert torch.equal(C, S), k
     nwords = 0
