@@ -284,31 +284,17 @@ def run_step(cases, data, ev_pairs=None, ext=None, stream=None, lane_streams=Non
                     ext.record(ev_pairs[k][1], stream)
         return
     if grouped is not None:
-        # the step's weights in one grouped sparsify call (one launch per (m, n) class), then the
-        # grouped SpMM (programmatic dependent launch: its prologue overlaps the sparsifier's tail)
-        classes = sorted({(c.m, c.n) for c in cases})
-        if lane_streams and len(classes) > 1:
-            # one grouped sparsify call per (m, n) class, the classes on separate streams
-            fork = torch.cuda.Event()
-            fork.record(stream)
-            for j, cl in enumerate(classes):
-                ls = lane_streams[j % len(lane_streams)]
-                ls.wait_event(fork)
-                with torch.cuda.stream(ls):
-                    sten.sparsify_grouped_nm_batched([(d["W"], c.n, c.m, c.g, d["values"], d["idx"])
-                                                      for c, d in zip(cases, data) if (c.m, c.n) == cl])
-            for ls in lane_streams[:len(classes)]:
-                stream.wait_stream(ls)
-        else:
-            with torch.cuda.stream(stream):
-                if ev_pairs is not None:
-                    for k in range(len(cases)):
-                        ext.record(ev_pairs[k][2], stream)
-                sten.sparsify_grouped_nm_batched([(d["W"], c.n, c.m, c.g, d["values"], d["idx"])
-                                                  for c, d in zip(cases, data)])
-                if ev_pairs is not None:
-                    for k in range(len(cases)):
-                        ext.record(ev_pairs[k][0], stream)
+        # the step's weights in ONE grouped sparsify launch (all (m, n) classes), then the grouped
+        # SpMM (programmatic dependent launch: its prologue overlaps the sparsifier's tail)
+        with torch.cuda.stream(stream):
+            if ev_pairs is not None:
+                for k in range(len(cases)):
+                    ext.record(ev_pairs[k][2], stream)
+            sten.sparsify_grouped_nm_batched([(d["W"], c.n, c.m, c.g, d["values"], d["idx"])
+                                              for c, d in zip(cases, data)])
+            if ev_pairs is not None:
+                for k in range(len(cases)):
+                    ext.record(ev_pairs[k][0], stream)
         with torch.cuda.stream(stream):
             if ev_pairs is not None:
                 ext.record(ev_pairs[0][3], stream)
@@ -550,9 +536,11 @@ def bench_sten(args, rank, world, local_rank):
                                                    sp24=(mode == "sp24"))
     in_step_spmm_ms = [sum(x) / len(x) for x in spmm_ms]
     in_step_spars_ms = [sum(x) / len(x) for x in spars_ms]
-    grouped_ms = None
+    grouped_ms = grouped_sp_ms = None
     if mode == "grouped":
         grouped_ms = in_step_spmm_ms[0] if args.profile else grouped_b2b(cases, sets, grouped)
+        # the step's ONE mixed sparsify launch, timed the same way (its b2b duration per launch)
+        grouped_sp_ms = None if args.profile else grouped_b2b(cases, sets, grouped, which="sparsify")
     if b2b is not None:
         spars_ms = [[t] * args.steps for t in b2b["sparsify_ms"]]
         if grouped_ms is None:
@@ -564,8 +552,8 @@ def bench_sten(args, rank, world, local_rank):
     spmm_total_ms = sum(sum(x) for x in spmm_ms)
     spmm_nz = sum(nz_flops(c) for c in cases) * args.steps
     spmm_bytes_tot = sum(spmm_bytes(c) for c in cases) * args.steps
-    launches_per_step = (len({(c.m, c.n) for c in cases}) + 1) if mode == "grouped" else \
-        (len({(c.m, c.n) for c in cases}) + 2 * len(cases)) if mode == "sp24" else sum(1 + sten.launch_count(d["plan"])
+    launches_per_step = 2 if mode == "grouped" else \
+        (1 + 2 * len(cases)) if mode == "sp24" else sum(1 + sten.launch_count(d["plan"])
                                                                         for d in sets[0])
     peaks = load_peaks()
     if dtype == "f32":
@@ -621,8 +609,8 @@ def bench_sten(args, rank, world, local_rank):
                             "sten_spmm_autotune per case (min of 5 timed launches per variant, before timing)",
                    "step": ("grouped sparsify (a1-a3), then per case the 2:4 pack and the K6 sparse tensor-core "
                             "SpMM (a5-a7), in one CUDA graph") if mode == "sp24" else
-                           ("grouped sparsify (a1-a3) of every weight (one launch per (m, n) class, the classes "
-                            "on separate streams), then ONE grouped split-K SpMM launch (a5-a7) of all cases "
+                           ("grouped sparsify (a1-a3) of every weight in ONE mixed launch (all (m, n) classes), "
+                            "then ONE grouped split-K SpMM launch (a5-a7) of all cases "
                             "(tile %d, automatic splits), in one CUDA graph" % GROUPED_TILE)
                            if mode == "grouped" else
                            "sparsify (a1-a3) + SpMM (a5-a7) per case; independent cases spread over %d "
@@ -637,13 +625,7 @@ def bench_sten(args, rank, world, local_rank):
                               "share: SpMM time over SpMM + sparsify time (pass 3; the ncu launch list's "
                               "share is the cross-check), else over the single-stream step"},
         "per_kernel_timing": (b2b or {}).get("how", "in-step event brackets of the single-stream graph (pass 2)"),
-        "sparsify": {"kernel": "sparsify_grouped_nm_kernel (a1-a3)", "bound": "hbm",
-                     "achieved": round(sum(sparsify_bytes(c) for c in cases) * args.steps
-                                       / (sum(sum(x) for x in spars_ms) * 1e-3) / 1e9, 1),
-                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": round(sum(sparsify_bytes(c) for c in cases) * args.steps
-                                   / (sum(sum(x) for x in spars_ms) * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
-                     "note": "algorithmic bytes M*K*s + M*K'*s + idx per launch over the per-launch time"},
+        "sparsify": sparsify_roofline(cases, spars_ms, grouped_sp_ms, peaks, args.steps),
         "per_case": per_case,
         "gpu_launches": launches_per_step * args.steps,
         "loop_ms_device": round(loop_ms, 3),
@@ -655,6 +637,25 @@ def bench_sten(args, rank, world, local_rank):
     # the timed step's results (every set holds the same inputs) for bench's own parity check
     gpu_out = [(d["idx"].cpu().numpy(), d["C"].float().cpu().numpy()) for d in sets[0]]
     return out, cases, host, dtype, g, gpu_out
+
+
+def sparsify_roofline(cases, spars_ms, grouped_sp_ms, peaks, steps):
+    """K1's HBM roofline: algorithmic bytes M*K*s + M*K'*s + idx over the launch time -- the step's ONE
+    mixed launch of every weight (grouped mode, b2b duration) or the per-case single launches."""
+    tot = sum(sparsify_bytes(c) for c in cases)
+    if grouped_sp_ms:
+        gbs = tot / (grouped_sp_ms * 1e-3) / 1e9
+        return {"kernel": "sparsify_grouped_nm_batched_kernel (a1-a3, one launch of all %d weights)" % len(cases),
+                "bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(gbs / peaks["hbm_gbs"], 4), "us_per_launch": round(grouped_sp_ms * 1e3, 2),
+                "algorithmic_bytes_per_launch": round(tot, 1),
+                "single_launch_frac": round(tot * steps / (sum(sum(x) for x in spars_ms) * 1e-3) / 1e9
+                                            / peaks["hbm_gbs"], 4),
+                "note": "frac: the mixed launch's b2b duration; single_launch_frac: one launch per weight (pass 3)"}
+    gbs = tot * steps / (sum(sum(x) for x in spars_ms) * 1e-3) / 1e9
+    return {"kernel": "sparsify_grouped_nm_kernel (a1-a3)", "bound": "hbm", "achieved": round(gbs, 1),
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(gbs / peaks["hbm_gbs"], 4),
+            "note": "algorithmic bytes M*K*s + M*K'*s + idx per launch over the per-launch time"}
 
 
 NVLINK_GBS = 770.0      # measured peer copy per direction (B200_PROFILING.md), the all-gather roofline term
@@ -890,22 +891,29 @@ GROUPED_TILE = 2        # the 16-warp 120 x 256 SIMT tile for every problem: fas
                         # mix (tile 0: tile 3 for 1:10) measured equal (tools/grouped_split_probe.py)
 
 
-def grouped_b2b(cases, sets, grouped):
-    """Pass 3 for the grouped step: the R input sets' grouped SpMM launches back to back in one
-    CUDA graph (R x set bytes > 3 x L2), CUDA events around the replay on its stream, median of
-    3 -> ms per launch."""
+def grouped_b2b(cases, sets, grouped, which="spmm"):
+    """Pass 3 for the grouped step: the R input sets' grouped SpMM (or grouped sparsify) launches
+    back to back in one CUDA graph (R x set bytes > 3 x L2), CUDA events around the replay on its
+    stream, median of 3 -> ms per launch."""
     import torch
     from paper_2304_07613_b200 import sten
     R = len(sets)
     st = torch.cuda.Stream()
+
+    def launch(r):
+        if which == "spmm":
+            sten.spmm_grouped_nm_batched_ex(grouped_problems(cases, sets[r]), grouped[r][1], None, grouped[r][0])
+        else:
+            sten.sparsify_grouped_nm_batched([(d["W"], c.n, c.m, c.g, d["values"], d["idx"])
+                                              for c, d in zip(cases, sets[r])])
     with torch.cuda.stream(st):
         for r in range(R):
-            sten.spmm_grouped_nm_batched_ex(grouped_problems(cases, sets[r]), grouped[r][1], None, grouped[r][0])
+            launch(r)
     torch.cuda.synchronize()
     gph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(gph, stream=st):
         for r in range(R):
-            sten.spmm_grouped_nm_batched_ex(grouped_problems(cases, sets[r]), grouped[r][1], None, grouped[r][0])
+            launch(r)
     gph.replay()
     torch.cuda.synchronize()
     ts = []

@@ -103,9 +103,9 @@ sten_status sten_sparsify_grouped_nm(sten_nmg f, sten_dtype dt,
                                      const void* W, int64_t M, int64_t K, int64_t ldw,
                                      void* values, uint8_t* idx, void* stream);
 
-/* Grouped sparsify: the weights of one step in as few launches as possible -- one launch per
- * (m, n-vector class) of the problems (e.g. 3 launches for the 9 C2 weights), each CTA working on
- * one problem exactly as sten_sparsify_grouped_nm does (same bits).  All problems share dt.
+/* Grouped sparsify: the weights of one step in ONE launch whatever their (n, m, g) (e.g. the 9 C2
+ * weights of three sparsity classes), each CTA working on one problem exactly as
+ * sten_sparsify_grouped_nm does (same bits).  All problems share dt.
  * count in [1, 12]; every problem is validated before any launch (errors as the single call). */
 typedef struct {
     sten_nmg f;

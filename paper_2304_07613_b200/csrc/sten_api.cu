@@ -93,33 +93,6 @@ bool dispatch_sparsify(int m, const void* W, int64_t ldw, int64_t G, int64_t KB,
     return false;
 }
 
-// grouped sparsify: the problems of one (T, m, NK) class in one launch
-template <typename T, int MB, int NK>
-void launch_sparsify_batch(const SparsifyBatch& bt, int blocks, cudaStream_t st) {
-    sparsify_grouped_nm_batched_kernel<T, MB, NK><<<unsigned(blocks), 256, 0, st>>>(bt);
-}
-
-template <typename T, int MB>
-void launch_sparsify_batch_nk(const SparsifyBatch& bt, int nk, int blocks, cudaStream_t st) {
-    if (nk == 1) launch_sparsify_batch<T, MB, 1>(bt, blocks, st);
-    else if (nk == 2) launch_sparsify_batch<T, MB, 2>(bt, blocks, st);
-    else launch_sparsify_batch<T, MB, 0>(bt, blocks, st);
-}
-
-template <typename T>
-bool dispatch_sparsify_batch(int m, const SparsifyBatch& bt, int nk, int blocks, cudaStream_t st) {
-    switch (m) {
-        case 2: launch_sparsify_batch_nk<T, 2>(bt, nk, blocks, st); return true;
-        case 4: launch_sparsify_batch_nk<T, 4>(bt, nk, blocks, st); return true;
-        case 6: launch_sparsify_batch_nk<T, 6>(bt, nk, blocks, st); return true;
-        case 8: launch_sparsify_batch_nk<T, 8>(bt, nk, blocks, st); return true;
-        case 10: launch_sparsify_batch_nk<T, 10>(bt, nk, blocks, st); return true;
-        case 12: launch_sparsify_batch_nk<T, 12>(bt, nk, blocks, st); return true;
-        case 16: launch_sparsify_batch_nk<T, 16>(bt, nk, blocks, st); return true;
-    }
-    return false;
-}
-
 template <typename T, int MB>
 void launch_densify(const void* values, const uint8_t* idx, int64_t M, int64_t KB, sten_nmg f,
                     int64_t Kp, void* W, int64_t ldw, bool aligned, cudaStream_t st) {
@@ -622,31 +595,34 @@ sten_status sten_sparsify_grouped_nm_batched(int32_t count, const sten_sparsify_
         nkc[p] = vec_ok(1) ? 1 : vec_ok(2) ? 2 : 0;
     }
     cudaStream_t st = as_stream(stream);
-    bool done[kMaxSparsifyBatch] = {false};
-    for (int p0 = 0; p0 < count; ++p0) {
-        if (done[p0]) continue;
-        // one launch per (m, NK) class, problems in the caller's order
-        SparsifyBatch bt;
-        memset(&bt, 0, sizeof(bt));
-        int blocks = 0;
-        for (int p = p0; p < count; ++p) {
-            if (done[p] || probs[p].f.m != probs[p0].f.m || nkc[p] != nkc[p0]) continue;
-            done[p] = true;
-            const sten_sparsify_problem& q = probs[p];
-            const int64_t G = q.M / q.f.g, KB = q.K / q.f.m;
-            if (G * KB == 0) continue;
-            const int c = bt.count++;
-            bt.W[c] = q.W; bt.values[c] = q.values; bt.idx[c] = q.idx;
-            bt.ldw[c] = q.ldw; bt.G[c] = G; bt.KB[c] = KB; bt.Kp[c] = KB * q.f.n;
-            bt.n[c] = q.f.n; bt.g[c] = q.f.g; bt.aligned[c] = al[p];
-            bt.block0[c] = blocks;
-            blocks += int(grid1d(G * KB));
-        }
-        if (bt.count == 0) continue;
-        bt.block0[bt.count] = blocks;
-        const bool ok = dt == STEN_F32 ? dispatch_sparsify_batch<float>(probs[p0].f.m, bt, nkc[p0], blocks, st)
-                                       : dispatch_sparsify_batch<bf16_t>(probs[p0].f.m, bt, nkc[p0], blocks, st);
-        if (!ok) return STEN_ERR_UNSUPPORTED;
+    // ONE launch for every problem; the lean instantiation when every problem has a lean body
+    SparsifyBatch bt;
+    memset(&bt, 0, sizeof(bt));
+    int64_t blocks = 0;
+    bool lean = true;
+    for (int p = 0; p < count; ++p) {
+        const sten_sparsify_problem& q = probs[p];
+        const int64_t G = q.M / q.f.g, KB = q.K / q.f.m;
+        if (G * KB == 0) continue;
+        const int c = bt.count++;
+        bt.W[c] = q.W; bt.values[c] = q.values; bt.idx[c] = q.idx;
+        bt.ldw[c] = q.ldw; bt.G[c] = G; bt.KB[c] = KB; bt.Kp[c] = KB * q.f.n;
+        bt.n[c] = q.f.n; bt.g[c] = q.f.g; bt.aligned[c] = al[p];
+        bt.m[c] = q.f.m; bt.nk[c] = nkc[p];
+        bt.block0[c] = int(blocks);
+        blocks += int64_t(grid1d(G * KB));
+        lean = lean && sparsify_lean_ok(q.f.m, nkc[p], al[p]);
+    }
+    if (bt.count == 0) return STEN_OK;
+    if (blocks > int64_t(0x7fffffff)) return STEN_ERR_UNSUPPORTED;
+    bt.block0[bt.count] = int(blocks);
+    const unsigned grid = unsigned(blocks);
+    if (dt == STEN_F32) {
+        if (lean) sparsify_grouped_nm_batched_kernel<float, 1><<<grid, 256, 0, st>>>(bt);
+        else sparsify_grouped_nm_batched_kernel<float, 0><<<grid, 256, 0, st>>>(bt);
+    } else {
+        if (lean) sparsify_grouped_nm_batched_kernel<bf16_t, 1><<<grid, 256, 0, st>>>(bt);
+        else sparsify_grouped_nm_batched_kernel<bf16_t, 0><<<grid, 256, 0, st>>>(bt);
     }
     return last_cuda();
 }

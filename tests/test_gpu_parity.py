@@ -549,6 +549,41 @@ def test_spmm_batched_equals_single_launches(tile):
         assert rel_err(C, C_ref, Bound) <= 1e-5
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("lean", [True, False])
+def test_sparsify_batched_mixed_classes_equals_oracle(dtype, lean):
+    """ONE grouped sparsify launch over mixed (n, m, g) equals the oracle bit for bit (idx and values)
+    for every problem.  lean: every problem has a vector-store body on aligned rows (the lean
+    instantiation: m in {2, 4, 8, 10}, n in {1, 2}); else the full one -- per-position stores
+    (n = 3, 5), element-aligned rows, m = 6 / 12 / 16, g from 1 to 16, ragged sizes."""
+    if lean:
+        specs = [(96, 3072, 2, 4, 4), (64, 768, 1, 4, 4), (40, 800, 1, 10, 4), (33, 80, 1, 2, 1),
+                 (36, 96, 2, 8, 3), (8, 40, 2, 4, 8), (24, 160, 1, 8, 8), (30, 120, 2, 10, 5)]
+    else:
+        specs = [(96, 3072, 2, 4, 4), (64, 768, 1, 4, 4), (40, 800, 1, 10, 4), (48, 96, 3, 6, 16),
+                 (33, 80, 1, 2, 1), (24, 160, 5, 16, 8), (36, 96, 2, 8, 3), (16, 72, 1, 12, 2),
+                 (8, 40, 2, 4, 8), (30, 66, 1, 6, 5)]
+    probs, refs, keep = [], [], []
+    for k, (M, K, n, m, g) in enumerate(specs):
+        W = synthetic.weights(M, K, seed=90 + k, dtype=dtype)
+        ld = K + (3 if (k % 3 == 2 and not lean) else 0)        # element-aligned rows for some problems
+        Wp = np.zeros((M, ld), dtype=W.dtype)
+        Wp[:, :K] = W
+        Wd = dev(Wp, dtype, ld_multiple=1)[:, :K]
+        Kp = K // m * n
+        tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+        vals = torch.full((M, Kp), float("nan"), dtype=tdt, device="cuda")
+        idx = torch.full((M // g, K // m, n), 255, dtype=torch.uint8, device="cuda")
+        probs.append((Wd, n, m, g, vals, idx))
+        refs.append(oracle.sparsify(W, n, m, g))
+        keep.append(Wp)
+    sten.sparsify_grouped_nm_batched(probs)
+    torch.cuda.synchronize()
+    for k, ((Wd, n, m, g, vals, idx), (v_ref, i_ref)) in enumerate(zip(probs, refs)):
+        assert np.array_equal(idx.cpu().numpy().reshape(i_ref.shape), i_ref), k
+        assert np.array_equal(host(vals), v_ref), k
+
+
 @pytest.mark.parametrize("tile", [0, 1, 2, 3])
 @pytest.mark.parametrize("splits", [None, [3, 2, 1, 5]])
 def test_spmm_batched_split_k_equals_cluster_split(tile, splits):
