@@ -43,6 +43,11 @@ __device__ unsigned long long g_sten_timing[16384][8];
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
             const unsigned cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);          \
             if (cta_ < 16384) g_sten_timing[cta_][i] = t_;                                               \
+            if (cta_ < 16384 && (i) == 0) {                                                               \
+                unsigned sm_;                                                                             \
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));                                          \
+                g_sten_timing[cta_][7] = sm_ + 1;                                                         \
+            }                                                                                             \
         }                                                                                                 \
     } while (0)
 // per-CTA accumulated cycles of named waits / phases (lane 0 of the warps that time them)
@@ -623,6 +628,7 @@ __device__ __forceinline__ void spmm_simt_body(const SpmmArgs& a, const CUtensor
         __shared__ unsigned last_flag;
         if (tid == 0) last_flag = atomicAdd(a.ctr + tile_lin, 1u) == unsigned(a.split - 1) ? 1u : 0u;
         __syncthreads();
+        STEN_TSTAMP(4);
         if (!last_flag) return;
         __threadfence();
         const float* tile0 = a.ws + tile_lin * a.split * int64_t(BM) * BN;
@@ -645,6 +651,7 @@ __device__ __forceinline__ void spmm_simt_body(const SpmmArgs& a, const CUtensor
             }
         }
         if (tid == 0) a.ctr[tile_lin] = 0u;                       // leave the counter at zero for the next call
+        STEN_TSTAMP(5);
         return;
     }
     // split-K: park the partial tile [BM][BN] (fp32) after the header, reduce over the cluster
