@@ -9,6 +9,7 @@ import os
 import shutil
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TAG = os.environ.get("TAG", "r02")        # r02b: the second profiling pass of round 2 (tools/profile_r02b.sh)
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 UNIT = {"ns": 1.0, "nsecond": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6,
@@ -33,7 +34,7 @@ def csv_rows(path):
 
 
 def launch_list():
-    rows = csv_rows(os.path.join(OUT, "r02_launches.csv"))
+    rows = csv_rows(os.path.join(OUT, TAG + "_launches.csv"))
     h = rows[0]
     I, K, N, U, V = (h.index(x) for x in ("ID", "Kernel Name", "Metric Name", "Metric Unit", "Metric Value"))
     per, names = collections.defaultdict(dict), {}
@@ -52,7 +53,7 @@ def launch_list():
 
 
 def full(name):
-    path = os.path.join(OUT, "r02_%s_raw.csv" % name)
+    path = os.path.join(OUT, "%s_%s_raw.csv" % (TAG, name))
     if not os.path.exists(path):
         return None
     rows = csv_rows(path)
@@ -75,13 +76,13 @@ def full(name):
 
 def main():
     ll = launch_list()
-    shutil.copy(os.path.join(OUT, "r02_launches.csv"), os.path.join(PROF, "ncu_r02_launches.csv"))
+    shutil.copy(os.path.join(OUT, TAG + "_launches.csv"), os.path.join(PROF, "ncu_%s_launches.csv" % TAG))
     summ = {"_what": "round 2, one B200: ncu launch list of `bench.py --profile --steps 2 --warmup 1 --no-graph` "
                      "(the grouped C2 step; serialised, cold: compare shares) and --set full captures "
-                     "(tools/profile_r02.sh)", "launch_list": ll}
+                     "(tools/profile_%s.sh)" % TAG, "launch_list": ll}
     for name in ("grouped", "gsparsify", "sp24", "sddmm", "nmgx"):
         summ[name] = full(name)
-    with open(os.path.join(PROF, "ncu_r02_summary.json"), "w") as f:
+    with open(os.path.join(PROF, "ncu_%s_summary.json" % TAG), "w") as f:
         json.dump(summ, f, indent=1)
     g = summ.get("grouped")
     if g and "dram__bytes_read.sum" in g:

@@ -43,6 +43,21 @@ if on("k1"):
     sten.sparsify_grouped_nm_batched([(Wd, n, m, g, vals, idx)])
     torch.cuda.synchronize()
     ok("k1 grouped sparsify", torch.equal(idx, i))
+    # one launch over mixed classes: the lean body set, then the full one (n = 3, element-aligned rows)
+    for specs in ([(64, 768, 2, 4, 4), (40, 800, 1, 10, 4), (32, 256, 2, 8, 8)],
+                  [(64, 768, 2, 4, 4), (48, 96, 3, 6, 16), (30, 66, 1, 6, 5)]):
+        probs, refs = [], []
+        for k, (Mq, Kq, nq, mq, gq) in enumerate(specs):
+            Wq = synthetic.weights(Mq, Kq, seed=50 + k)
+            probs.append((dev(Wq, "f32", ld_multiple=1 if Kq % 4 else 4), nq, mq, gq,
+                          torch.empty((Mq, Kq // mq * nq), device="cuda"),
+                          torch.empty((Mq // gq, Kq // mq, nq), dtype=torch.uint8, device="cuda")))
+            refs.append(oracle.sparsify(Wq, nq, mq, gq))
+        sten.sparsify_grouped_nm_batched(probs)
+        torch.cuda.synchronize()
+        ok("k1 grouped sparsify mixed %d" % len(specs[1]),
+           all(np.array_equal(p[5].cpu().numpy().reshape(r[1].shape), r[1]) and np.array_equal(p[4].cpu().numpy(), r[0])
+               for p, r in zip(probs, refs)))
     D = sten.densify(v, i, n, m, g, K)
     torch.cuda.synchronize()
     ok("k2 densify", np.array_equal(D.cpu().numpy(), oracle.densify(v_ref, i_ref, n, m, g, K)))
