@@ -140,6 +140,9 @@ constexpr SimtTile kSimtTiles[8] = {{0, 0, 0, 0},   {8, 8, 56, 2}, {16, 8, 120, 
                                     {8, 4, 112, 2}, {8, 4, 56, 2}, {8, 4, 56, 3},   {12, 4, 88, 2}};
 constexpr int kSimtNumTiles = 7;
 constexpr int kMaxSplit = 8;              // portable thread-block cluster size
+#ifndef STEN_SLAB_COST
+#define STEN_SLAB_COST 6.0
+#endif
 
 inline bool simt_tile_ok(int tile, sten_dtype ab) {
     if (tile < 1 || tile > kSimtNumTiles) return false;
@@ -803,11 +806,17 @@ sten_status sten_spmm_grouped_nm_batched_ex(int32_t count, const sten_spmm_probl
             ctr += tiles;
         }
     }
-    // longest unit (K' / S) first: the block scheduler then fills the tail with short units
+    // longest unit first: the block scheduler then fills the tail with short units.  A unit's time
+    // ~ its kept k plus a fixed cost per K-slab (barrier round trip, idx words, row addresses: ~6 kept
+    // k, from the per-class efficiencies of section 14), so 1:10 units (4 kept per slab) count longer
+    // than their K' alone says
     int order[kMaxBatch];
     for (int p = 0; p < count; ++p) order[p] = p;
-    std::stable_sort(order, order + count,
-                     [&](int x, int y) { return as[x].Kp / as[x].split > as[y].Kp / as[y].split; });
+    auto unit_cost = [&](int x) {
+        const double slabs = double((as[x].KB + as[x].kbs - 1) / as[x].kbs);
+        return (double(as[x].Kp) + STEN_SLAB_COST * slabs) / as[x].split;
+    };
+    std::stable_sort(order, order + count, [&](int x, int y) { return unit_cost(x) > unit_cost(y); });
     SpmmArgs sorted[kMaxBatch];
     int tiles_of[kMaxBatch];
     int live = 0;
