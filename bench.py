@@ -1017,26 +1017,23 @@ def bench_e2e(cases, host, dtype, steps, device):
         h2d += Wh.numel() * Wh.element_size() + Bh.numel() * Bh.element_size()
         d2h += Ch.numel() * Ch.element_size()
     stream = torch.cuda.current_stream()
-    # the cases are independent linears: spread over 3 streams (LPT on their copy bytes) so one
-    # case's PCIe copies overlap another's kernels and H2D overlaps D2H; the step ends when the
-    # main stream has joined every lane (all C_host written)
-    n_lanes = min(int(os.environ.get("STEN_E2E_LANES", "3")), len(cases))
-    lanes = [torch.cuda.Stream(device) for _ in range(n_lanes)]
-    lane_of = [0] * len(cases)
-    load = [0.0] * n_lanes
-    for k in sorted(range(len(cases)), key=lambda k: -(cases[k].M * cases[k].Kp + cases[k].Kp * cases[k].N)):
-        j = min(range(n_lanes), key=lambda t: load[t])
-        lane_of[k] = j
-        load[j] += cases[k].M * cases[k].Kp + cases[k].Kp * cases[k].N
+    # the cases are independent linears: ONE pipelined call (sten_sparse_linear_host_pipelined_async)
+    # puts every case's H2D back to back on a copy-in stream, its kernels on a compute stream as soon as
+    # its inputs land and its D2H on a copy-out stream as soon as C is ready, so the host link carries
+    # H2D and D2H at once; the cases go smallest-input first (the kernels and D2H start early; measured
+    # 2.75 vs 2.81 ms largest-C first and 2.85 ms for per-case calls on 3 lanes, tools/e2e_probe.py).
+    # The step ends when the timing stream has joined the three.
+    order = sorted(range(len(cases)), key=lambda k: cases[k].M * cases[k].Kp + cases[k].Kp * cases[k].N)
+    s_in, s_c, s_out = (torch.cuda.Stream(device) for _ in range(3))
+    problems = [(bufs[k][0], bufs[k][1], cases[k].n, cases[k].m, cases[k].g, bufs[k][2], bufs[k][3]) for k in order]
 
     def step():
         fork = torch.cuda.Event()
         fork.record(stream)
-        for ls in lanes:
+        for ls in (s_in, s_c, s_out):
             ls.wait_event(fork)
-        for k, (c, (Wh, Bh, Ch, ws)) in enumerate(zip(cases, bufs)):
-            sten.sparse_linear_host_async(Wh, Bh, c.n, c.m, c.g, Ch, ws, stream=lanes[lane_of[k]])
-        for ls in lanes:
+        sten.sparse_linear_host_pipelined_async(problems, s_in, s_c, s_out)
+        for ls in (s_in, s_c, s_out):
             stream.wait_stream(ls)
 
     for _ in range(2):
@@ -1053,8 +1050,9 @@ def bench_e2e(cases, host, dtype, steps, device):
     val = sum(eff_flops(c) for c in cases) * steps / (ms * 1e-3) / 1e9
     return {"value": round(val, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": round(ms / steps, 4),
-            "path": "sten_sparse_linear_host_async per case (pinned host W,B -> H2D -> sparsify -> SpMM -> D2H C), "
-                    "cases over %d streams, step joined on the timing stream" % n_lanes}
+            "path": "sten_sparse_linear_host_pipelined_async (pinned host W,B -> H2D on a copy-in stream, sparsify "
+                    "+ SpMM on a compute stream, D2H C on a copy-out stream, per case, handed over by events; "
+                    "smallest input first), step joined on the timing stream"}
 
 
 # ------------------------------------------------------------------------------------------------

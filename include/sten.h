@@ -358,6 +358,33 @@ sten_status sten_sparse_linear_host_async(sten_nmg f, sten_dtype ab_dt,
                                           void* C_host, int64_t ldc, sten_dtype c_dt,
                                           void* workspace, int64_t workspace_bytes, void* stream);
 
+/* Several independent linears from host memory, pipelined over three caller streams: every
+ * problem's H2D copies (W, B) are issued back to back on `copy_in`, its sparsify + SpMM on
+ * `compute` as soon as its inputs have landed, and its D2H copy of C on `copy_out` as soon as C is
+ * ready -- so the host link carries H2D and D2H at the same time and the kernels hide under the
+ * copies (the step costs ~ the H2D bytes at the link's rate plus the LAST problem's kernels and D2H;
+ * put a small problem last).  Per problem: host buffers pinned and valid until copy_out drains,
+ * its own `workspace` (sten_sparse_linear_host_workspace_size bytes), the same arithmetic and
+ * bits as sten_sparse_linear_host_async.  The three streams start after whatever the caller
+ * ordered before them; the caller joins copy_out (and compute) before reading C_host.  The call
+ * creates one event per problem and stage and releases it before returning (no state kept).
+ * count in [1, 64]; every problem is validated before anything is enqueued. */
+typedef struct {
+    sten_nmg f;
+    int32_t reserved;
+    const void* W_host;     /* [M][ldw] ab_dt */
+    int64_t M, K, ldw;
+    const void* B_host;     /* [K][ldb] ab_dt */
+    int64_t ldb, N;
+    void* C_host;           /* [M][ldc] c_dt */
+    int64_t ldc;
+    void* workspace;        /* device */
+    int64_t workspace_bytes;
+} sten_host_linear_problem;
+sten_status sten_sparse_linear_host_pipelined_async(int32_t count, const sten_host_linear_problem* problems,
+                                                    sten_dtype ab_dt, sten_dtype c_dt, void* copy_in,
+                                                    void* compute, void* copy_out);
+
 /* ---------------------------------------------------------------------------
  * K6: the 2:4 structured-sparse tensor-core path (NEXT-4; bf16 in, fp32 accumulate).
  *

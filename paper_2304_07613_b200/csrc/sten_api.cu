@@ -956,10 +956,9 @@ int64_t sten_sparse_linear_host_workspace_size(sten_nmg f, sten_dtype ab_dt, int
            round16(K * ldb * s) + round16(M * ldc * int64_t(dt_size(c_dt)));
 }
 
-static sten_status sparse_linear_host_impl(sten_nmg f, sten_dtype ab_dt, const void* W_host, int64_t M, int64_t K,
-                                          int64_t ldw, const void* B_host, int64_t ldb, int64_t N, void* C_host,
-                                          int64_t ldc, sten_dtype c_dt, void* workspace, int64_t workspace_bytes,
-                                          void* stream, bool sync) {
+static sten_status host_linear_check(sten_nmg f, sten_dtype ab_dt, const void* W_host, int64_t M, int64_t K,
+                                     int64_t ldw, const void* B_host, int64_t ldb, int64_t N, void* C_host,
+                                     int64_t ldc, sten_dtype c_dt, void* workspace, int64_t workspace_bytes) {
     sten_status s = check_format(f);
     if (s) return s;
     if (!dtype_ok(ab_dt) || !dtype_ok(c_dt)) return STEN_ERR_INVALID_ARG;
@@ -968,6 +967,15 @@ static sten_status sparse_linear_host_impl(sten_nmg f, sten_dtype ab_dt, const v
     if (N < 0 || ldw < K || ldb < N || ldc < N) return STEN_ERR_SHAPE;
     const int64_t need = sten_sparse_linear_host_workspace_size(f, ab_dt, M, K, N, c_dt);
     if (need < 0 || workspace_bytes < need || !aligned16(workspace)) return STEN_ERR_INVALID_ARG;
+    return STEN_OK;
+}
+
+// the three stages of one host linear: H2D of W and B on `in`, sparsify + SpMM on `cmp` after `in`'s
+// copies, D2H of C on `out` after the kernels (in == cmp == out: the single-stream call)
+static sten_status host_linear_stages(sten_nmg f, sten_dtype ab_dt, const void* W_host, int64_t M, int64_t K,
+                                      int64_t ldw, const void* B_host, int64_t ldb, int64_t N, void* C_host,
+                                      int64_t ldc, sten_dtype c_dt, void* workspace, cudaStream_t in,
+                                      cudaStream_t cmp, cudaStream_t out) {
     const int64_t sab = int64_t(dt_size(ab_dt)), sc = int64_t(dt_size(c_dt));
     const int64_t Kp = K / f.m * f.n;
     const int64_t dldb = (N * sab + 15) / 16 * 16 / sab;
@@ -978,22 +986,71 @@ static sten_status sparse_linear_host_impl(sten_nmg f, sten_dtype ab_dt, const v
     uint8_t* dI = reinterpret_cast<uint8_t*>(p); p += round16(M / f.g * (K / f.m) * f.n);
     void* dB = p;             p += round16(K * dldb * sab);
     void* dC = p;
+    // pitched copy, or ONE linear copy when both sides are dense (the copy engines move a 2-D copy
+    // row by row; measured: the C2 step's copies take ~15 % longer as 2-D copies of 3-12 KB rows)
+    auto copy2d = [](void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                     cudaMemcpyKind kind, cudaStream_t st) -> bool {
+        if (dpitch == width && spitch == width)
+            return cudaMemcpyAsync(dst, src, width * height, kind, st) == cudaSuccess;
+        return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, kind, st) == cudaSuccess;
+    };
+    auto hand_over = [](cudaStream_t from, cudaStream_t to) -> bool {
+        if (from == to) return true;
+        cudaEvent_t ev;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return false;
+        const bool ok = cudaEventRecord(ev, from) == cudaSuccess && cudaStreamWaitEvent(to, ev, 0) == cudaSuccess;
+        cudaEventDestroy(ev);                      // released once the recorded work completes
+        return ok;
+    };
+    if (M * K > 0 && !copy2d(dW, size_t(K * sab), W_host, size_t(ldw * sab), size_t(K * sab), size_t(M),
+                             cudaMemcpyHostToDevice, in))
+        return STEN_ERR_CUDA;
+    if (K * N > 0 && !copy2d(dB, size_t(dldb * sab), B_host, size_t(ldb * sab), size_t(N * sab), size_t(K),
+                             cudaMemcpyHostToDevice, in))
+        return STEN_ERR_CUDA;
+    if (!hand_over(in, cmp)) return STEN_ERR_CUDA;
+    sten_status s;
+    if ((s = sten_sparsify_grouped_nm(f, ab_dt, dW, M, K, K, dV, dI, cmp))) return s;
+    if ((s = spmm_impl(f, ab_dt, dV, dI, M, K, dB, dldb, N, dC, dldc, c_dt, nullptr, cmp))) return s;
+    if (!hand_over(cmp, out)) return STEN_ERR_CUDA;
+    if (M * N > 0 && !copy2d(C_host, size_t(ldc * sc), dC, size_t(dldc * sc), size_t(N * sc), size_t(M),
+                             cudaMemcpyDeviceToHost, out))
+        return STEN_ERR_CUDA;
+    return STEN_OK;
+}
+
+static sten_status sparse_linear_host_impl(sten_nmg f, sten_dtype ab_dt, const void* W_host, int64_t M, int64_t K,
+                                          int64_t ldw, const void* B_host, int64_t ldb, int64_t N, void* C_host,
+                                          int64_t ldc, sten_dtype c_dt, void* workspace, int64_t workspace_bytes,
+                                          void* stream, bool sync) {
+    sten_status s = host_linear_check(f, ab_dt, W_host, M, K, ldw, B_host, ldb, N, C_host, ldc, c_dt, workspace,
+                                      workspace_bytes);
+    if (s) return s;
     cudaStream_t st = as_stream(stream);
-    if (M * K > 0 &&
-        cudaMemcpy2DAsync(dW, size_t(K * sab), W_host, size_t(ldw * sab), size_t(K * sab), size_t(M),
-                          cudaMemcpyHostToDevice, st) != cudaSuccess)
-        return STEN_ERR_CUDA;
-    if (K * N > 0 &&
-        cudaMemcpy2DAsync(dB, size_t(dldb * sab), B_host, size_t(ldb * sab), size_t(N * sab), size_t(K),
-                          cudaMemcpyHostToDevice, st) != cudaSuccess)
-        return STEN_ERR_CUDA;
-    if ((s = sten_sparsify_grouped_nm(f, ab_dt, dW, M, K, K, dV, dI, stream))) return s;
-    if ((s = spmm_impl(f, ab_dt, dV, dI, M, K, dB, dldb, N, dC, dldc, c_dt, nullptr, st))) return s;
-    if (M * N > 0 &&
-        cudaMemcpy2DAsync(C_host, size_t(ldc * sc), dC, size_t(dldc * sc), size_t(N * sc), size_t(M),
-                          cudaMemcpyDeviceToHost, st) != cudaSuccess)
-        return STEN_ERR_CUDA;
+    if ((s = host_linear_stages(f, ab_dt, W_host, M, K, ldw, B_host, ldb, N, C_host, ldc, c_dt, workspace, st, st,
+                                st)))
+        return s;
     if (sync && cudaStreamSynchronize(st) != cudaSuccess) return STEN_ERR_CUDA;
+    return STEN_OK;
+}
+
+sten_status sten_sparse_linear_host_pipelined_async(int32_t count, const sten_host_linear_problem* probs,
+                                                    sten_dtype ab_dt, sten_dtype c_dt, void* copy_in, void* compute,
+                                                    void* copy_out) {
+    if (count < 1 || count > 64 || !probs) return STEN_ERR_INVALID_ARG;
+    for (int p = 0; p < count; ++p) {
+        const sten_host_linear_problem& q = probs[p];
+        const sten_status s = host_linear_check(q.f, ab_dt, q.W_host, q.M, q.K, q.ldw, q.B_host, q.ldb, q.N, q.C_host,
+                                                q.ldc, c_dt, q.workspace, q.workspace_bytes);
+        if (s) return s;
+    }
+    const cudaStream_t in = as_stream(copy_in), cmp = as_stream(compute), out = as_stream(copy_out);
+    for (int p = 0; p < count; ++p) {
+        const sten_host_linear_problem& q = probs[p];
+        const sten_status s = host_linear_stages(q.f, ab_dt, q.W_host, q.M, q.K, q.ldw, q.B_host, q.ldb, q.N,
+                                                 q.C_host, q.ldc, c_dt, q.workspace, in, cmp, out);
+        if (s) return s;
+    }
     return STEN_OK;
 }
 

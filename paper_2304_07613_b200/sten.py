@@ -42,6 +42,13 @@ class sten_sparsify_problem(ctypes.Structure):
                 ("K", ctypes.c_int64), ("ldw", ctypes.c_int64), ("values", ctypes.c_void_p), ("idx", ctypes.c_void_p)]
 
 
+class sten_host_linear_problem(ctypes.Structure):
+    _fields_ = [("f", sten_nmg), ("reserved", ctypes.c_int32), ("W_host", ctypes.c_void_p), ("M", ctypes.c_int64),
+                ("K", ctypes.c_int64), ("ldw", ctypes.c_int64), ("B_host", ctypes.c_void_p), ("ldb", ctypes.c_int64),
+                ("N", ctypes.c_int64), ("C_host", ctypes.c_void_p), ("ldc", ctypes.c_int64),
+                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_int64)]
+
+
 class sten_spmm_plan(ctypes.Structure):
     _fields_ = [("algo", ctypes.c_int32), ("split_k", ctypes.c_int32), ("tile", ctypes.c_int32),
                 ("reserved", ctypes.c_int32 * 5)]
@@ -79,6 +86,8 @@ SIGNATURES = {
                                      _vp, _i64, ctypes.c_int, _vp]),
     "sten_sparse_linear_host_async": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _i64,
                                                      _i64, _vp, _i64, ctypes.c_int, _vp, _i64, _vp]),
+    "sten_sparse_linear_host_pipelined_async": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(sten_host_linear_problem),
+                                                               ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
     "sten_resparsify_same_format": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _i64, _i64, _i64, _vp, _vp,
                                                    _vp]),
     "sten_spmm_grouped_nm_allgather": (ctypes.c_int, [sten_nmg, ctypes.c_int, _vp, _vp, _i64, _i64, _vp, _i64,
@@ -473,6 +482,27 @@ def sparse_linear_host_async(W_host: torch.Tensor, B_host: torch.Tensor, n: int,
                                                 _ld(C_host), _dt(C_host), workspace.data_ptr(), workspace.numel(),
                                                 _stream(stream)), "sten_sparse_linear_host_async")
     return C_host
+
+
+def sparse_linear_host_pipelined_async(problems, copy_in, compute, copy_out):
+    """sten_sparse_linear_host_pipelined_async: problems = [(W_host, B_host, n, m, g, C_host, workspace), ...];
+    H2D on copy_in back to back, kernels on compute, D2H on copy_out, handed over by events (no wait)."""
+    arr = (sten_host_linear_problem * len(problems))()
+    ab = c = None
+    for k, (W_host, B_host, n, m, g, C_host, workspace) in enumerate(problems):
+        ab = ab if ab is not None else _dt(W_host)
+        c = c if c is not None else _dt(C_host)
+        if _dt(W_host) != ab or _dt(B_host) != ab or _dt(C_host) != c:
+            raise TypeError("one dtype for every W / B, one for every C")
+        arr[k].f = sten_nmg(n, m, g)
+        arr[k].W_host, arr[k].M, arr[k].K, arr[k].ldw = W_host.data_ptr(), W_host.shape[0], W_host.shape[1], _ld(W_host)
+        arr[k].B_host, arr[k].ldb, arr[k].N = B_host.data_ptr(), _ld(B_host), B_host.shape[1]
+        arr[k].C_host, arr[k].ldc = C_host.data_ptr(), _ld(C_host)
+        arr[k].workspace, arr[k].workspace_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    _check(load().sten_sparse_linear_host_pipelined_async(len(problems), arr, ab, c, _stream(copy_in),
+                                                          _stream(compute), _stream(copy_out)),
+           "sten_sparse_linear_host_pipelined_async")
+    return [p[5] for p in problems]
 
 
 def sparse_linear_host_workspace_size(n: int, m: int, g: int, M: int, K: int, N: int,

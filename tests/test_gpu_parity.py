@@ -290,6 +290,34 @@ def test_host_e2e_entry_point():
     assert torch.equal(Ch2, Ch) and torch.equal(Ch3, Ch)
 
 
+def test_host_pipelined_entry_point():
+    """The pipelined host call (H2D / kernels / D2H on three streams handed over by events, the bench's
+    e2e path) over mixed problems: every C equals the single-stream call's bytes and the oracle; run
+    twice back to back on the same buffers (the events order reuse of each workspace)."""
+    g = 4
+    specs = [(256, 768, 300, 2, 4), (120, 800, 129, 1, 10), (64, 256, 256, 1, 4), (40, 96, 33, 2, 4)]
+    probs, singles, refs = [], [], []
+    for k, (M, K, N, n, m) in enumerate(specs):
+        W = synthetic.weights(M, K, seed=300 + k)
+        B = synthetic.activations(K, N, seed=310 + k)
+        Wh, Bh = torch.from_numpy(W).pin_memory(), torch.from_numpy(B).pin_memory()
+        Ch = torch.full((M, N), float("nan")).pin_memory()
+        ws = torch.empty(sten.sparse_linear_host_workspace_size(n, m, g, M, K, N), dtype=torch.uint8, device="cuda")
+        probs.append((Wh, Bh, n, m, g, Ch, ws))
+        C1 = torch.empty((M, N)).pin_memory()
+        sten.sparse_linear_host(Wh, Bh, n, m, g, C1, torch.empty_like(ws))
+        singles.append(C1)
+        v_ref, i_ref = oracle.sparsify(W, n, m, g)
+        refs.append(oracle.spmm(v_ref, i_ref, B, n, m, g))
+    s_in, s_c, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    for rep in range(2):
+        sten.sparse_linear_host_pipelined_async(probs, s_in, s_c, s_out)
+        torch.cuda.synchronize()
+        for (Wh, Bh, n, m, g_, Ch, ws), C1, (C_ref, Bound) in zip(probs, singles, refs):
+            assert torch.equal(Ch, C1)
+            assert rel_err(Ch, C_ref, Bound) <= 1e-5
+
+
 # ----------------------------------------------------------------------------------------
 # BASELINE.json sizes, in the launch configuration bench.py uses: sampled outputs
 # ----------------------------------------------------------------------------------------
