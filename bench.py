@@ -563,6 +563,11 @@ def bench_sten(args, rank, world, local_rank):
                 "frac": round(achieved / peak, 4), "traffic": measured_traffic(cfg, dtype, mode),
                 "algorithmic_bytes_per_launch": round(sum(spmm_bytes(c) for c in cases) / len(cases), 1),
                 "peak_source": peaks["fp32_source"],
+                "measured_ceiling": peaks.get("ffma2_ceiling"),
+                "frac_of_measured_ceiling": round(achieved / peaks["ffma2_ceiling"], 4)
+                if peaks.get("ffma2_ceiling") else None,
+                "ceiling_source": "register-only FFMA2 outer product of the inner loop's form, "
+                                  "profiles/microbench_r02_ffma2.jsonl (context; frac is against the derived peak)",
                 "kernel": ("spmm_simt_batched(2)_kernel (one grouped split-K launch of the step's %d SpMMs, "
                            "CUDA-core FFMA2)" % len(cases)) if mode == "grouped" else "spmm_simt_kernel (CUDA-core FFMA)"}
     else:
@@ -981,6 +986,10 @@ def load_peaks():
     # FP32 CUDA-core peak derived from unit counts and clock
     peaks["fp32_tflops"] = NUM_SMS * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
     peaks["fp32_source"] = "derived: 148 SM x 128 FP32 lanes x 2 flop x %.0f MHz" % sm_mhz
+    mb = os.path.join(ROOT, "profiles", "microbench_r02_ffma2.jsonl")
+    if os.path.exists(mb):
+        with open(mb) as f:
+            peaks["ffma2_ceiling"] = json.loads(f.readline()).get("ceiling_tflops")
     return peaks
 
 
