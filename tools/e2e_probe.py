@@ -63,3 +63,24 @@ probs = [bufs[k] for k in by_c]
 out["pipe_two_triples"] = timed(forked(tri + tri2, lambda: (sten.sparse_linear_host_pipelined_async(probs[0::2], *tri),
                                                             sten.sparse_linear_host_pipelined_async(probs[1::2], *tri2))))
 print(json.dumps(out))
+# the same copies as the pipelined call without the kernels (copy-in stream, copy-out stream)
+dev_in = [(torch.empty(p[0].shape, device="cuda"), torch.empty(p[1].shape, device="cuda"),
+           torch.empty(p[5].shape, device="cuda")) for p in bufs]
+
+
+def copies_only():
+    ev = torch.cuda.Event()
+    ev.record(main)
+    tri[0].wait_event(ev)
+    tri[2].wait_event(ev)
+    for k in by_in:
+        with torch.cuda.stream(tri[0]):
+            dev_in[k][0].copy_(bufs[k][0], non_blocking=True)
+            dev_in[k][1].copy_(bufs[k][1], non_blocking=True)
+        with torch.cuda.stream(tri[2]):
+            bufs[k][5].copy_(dev_in[k][2], non_blocking=True)
+    main.wait_stream(tri[0])
+    main.wait_stream(tri[2])
+
+
+print(json.dumps({"copies_only_27": timed(copies_only)}))
