@@ -492,8 +492,11 @@ __device__ __forceinline__ void spmm_simt_body(const SpmmArgs& a, const CUtensor
                 // in block kg KU / n + t / n, so its row address is base_t[t] + idx_byte(t) ROWB with
                 // base_t advanced by one k-step per iteration -- a byte permute and a shift-add per
                 // kept k.  Otherwise: block b = kk / n by multiply-shift, padded slots read a zero row.
-                auto kloop = [&](auto fast_tag) {
+                auto kloop = [&](auto fast_tag, auto aligned_tag) {
                     constexpr bool FAST = decltype(fast_tag)::value;
+                    // ALIGNED: every sub-block's idx bytes start on a word (gbase % 4 == 0, e.g. all C2
+                    // shapes), so a k-step's KU = 4 bytes are ONE word: no second load, no funnel shift
+                    constexpr bool ALIGNED = decltype(aligned_tag)::value && KU == 4;
                     uint32_t base_t[KU];
 #pragma unroll
                     for (int t = 0; t < KU; ++t) base_t[t] = bbase + lane_off + uint32_t(tb[t]);
@@ -503,10 +506,14 @@ __device__ __forceinline__ void spmm_simt_body(const SpmmArgs& a, const CUtensor
                         for (int q = 0; q < SUB; ++q) {
                             uint32_t offs[KU];
                             {
-                                const int o = imis[q] + kg * KU;
-                                const uint32_t wa = iaddr[q] + uint32_t(o & ~3);
-                                const uint32_t x =
-                                    __funnelshift_r(lds32_addr(wa), lds32_addr(wa + 4u), uint32_t(o & 3) * 8u);
+                                uint32_t x;
+                                if constexpr (ALIGNED) {
+                                    x = lds32_addr(iaddr[q] + uint32_t(kg) * 4u);
+                                } else {
+                                    const int o = imis[q] + kg * KU;
+                                    const uint32_t wa = iaddr[q] + uint32_t(o & ~3);
+                                    x = __funnelshift_r(lds32_addr(wa), lds32_addr(wa + 4u), uint32_t(o & 3) * 8u);
+                                }
                                 if constexpr (FAST) {
 #pragma unroll
                                     for (int t = 0; t < KU; ++t)
@@ -563,8 +570,15 @@ __device__ __forceinline__ void spmm_simt_body(const SpmmArgs& a, const CUtensor
                         }
                     }
                 };
-                if (n_divides_ku && ks % KU == 0) kloop(std::true_type{});
-                else kloop(std::false_type{});
+                bool idx_aligned = true;
+#pragma unroll
+                for (int q = 0; q < SUB; ++q) idx_aligned = idx_aligned && imis[q] == 0;
+                if (n_divides_ku && ks % KU == 0) {
+                    if (idx_aligned) kloop(std::true_type{}, std::true_type{});
+                    else kloop(std::true_type{}, std::false_type{});
+                } else {
+                    kloop(std::false_type{}, std::false_type{});
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[buf]);
