@@ -646,6 +646,37 @@ def test_spmm_batched_split_k_equals_cluster_split(tile, splits):
     assert torch.count_nonzero(ws[: 4].view(torch.int32)) == 0 or nb == 0
 
 
+def test_grouped_c2_problem_set():
+    """The C2 step's 9 problems through the grouped split-K launch with automatic splits (the bench's
+    launch) vs the oracle on sampled columns of every case, twice on one workspace (the tile counters
+    are left at zero), the same bits both times."""
+    cases = synthetic.config_cases(1, g=4, dtype="f32")
+    probs, host_in = [], []
+    for k, c in enumerate(cases):
+        W = synthetic.weights(c.M, c.K, seed=1234 + k, k_pad=c.k_pad)
+        B = synthetic.activations(c.K, c.N, seed=1234 + k, k_pad=c.k_pad)
+        v, i = gpu_sparsify(W, c.n, c.m, c.g, "f32")
+        probs.append((v, i, dev(B, "f32"), c.n, c.m, c.g, torch.full((c.M, c.N), float("nan"), device="cuda")))
+        host_in.append((W, B))
+    nb = sten.batched_workspace_size(probs, None, 2)
+    ws = torch.zeros(max(nb, 16) // 4 + 4, dtype=torch.float32, device="cuda")
+    outs = []
+    for rep in range(2):
+        for p in probs:
+            p[6].fill_(float("nan"))
+        sten.spmm_grouped_nm_batched_ex(probs, ws, None, 2)
+        torch.cuda.synchronize()
+        outs.append([p[6].clone() for p in probs])
+    assert all(torch.equal(a, b) for a, b in zip(outs[0], outs[1]))
+    cols = np.array([0, 1, 255, 256, 511, 700, 1023])
+    for k, (c, (W, B)) in enumerate(zip(cases, host_in)):
+        v_ref, i_ref = oracle.sparsify(W, c.n, c.m, c.g)
+        C_ref, Bound = oracle.spmm(v_ref, i_ref, np.ascontiguousarray(B[:, cols]), c.n, c.m, c.g,
+                                   nthreads=oracle.max_threads())
+        C = outs[0][k][:, torch.from_numpy(cols).cuda()]
+        assert rel_err(C, C_ref, Bound) <= 1e-5, c.label()
+
+
 def test_new_entry_points_reject_bad_arguments():
     """Argument errors of the fused / grouped entry points are returned before any launch."""
     n, m, g, M, K, N = 2, 4, 4, 32, 64, 40
