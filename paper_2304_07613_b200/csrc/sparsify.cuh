@@ -350,8 +350,12 @@ STEN_DEVICE_INLINE void sparsify_grouped_item(const SparsifyBatch& bt, int p, in
 #undef STEN_SP_BODY
 }
 
+#ifndef STEN_SP_BATCH_THREADS
+#define STEN_SP_BATCH_THREADS 128
+#endif
+constexpr int kSpBatchThreads = STEN_SP_BATCH_THREADS;     // threads per CTA of the grouped launch
 template <typename T, int LEAN>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kSpBatchThreads)
 sparsify_grouped_nm_batched_kernel(const __grid_constant__ SparsifyBatch bt) {
     // let a programmatically dependent SpMM launch now: its prologue overlaps this grid
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");

@@ -613,7 +613,7 @@ sten_status sten_sparsify_grouped_nm_batched(int32_t count, const sten_sparsify_
         bt.n[c] = q.f.n; bt.g[c] = q.f.g; bt.aligned[c] = al[p];
         bt.m[c] = q.f.m; bt.nk[c] = nkc[p];
         bt.block0[c] = int(blocks);
-        blocks += int64_t(grid1d(G * KB));
+        blocks += (G * KB + kSpBatchThreads - 1) / kSpBatchThreads;
         lean = lean && sparsify_lean_ok(q.f.m, nkc[p], al[p]);
     }
     if (bt.count == 0) return STEN_OK;
@@ -621,11 +621,11 @@ sten_status sten_sparsify_grouped_nm_batched(int32_t count, const sten_sparsify_
     bt.block0[bt.count] = int(blocks);
     const unsigned grid = unsigned(blocks);
     if (dt == STEN_F32) {
-        if (lean) sparsify_grouped_nm_batched_kernel<float, 1><<<grid, 256, 0, st>>>(bt);
-        else sparsify_grouped_nm_batched_kernel<float, 0><<<grid, 256, 0, st>>>(bt);
+        if (lean) sparsify_grouped_nm_batched_kernel<float, 1><<<grid, kSpBatchThreads, 0, st>>>(bt);
+        else sparsify_grouped_nm_batched_kernel<float, 0><<<grid, kSpBatchThreads, 0, st>>>(bt);
     } else {
-        if (lean) sparsify_grouped_nm_batched_kernel<bf16_t, 1><<<grid, 256, 0, st>>>(bt);
-        else sparsify_grouped_nm_batched_kernel<bf16_t, 0><<<grid, 256, 0, st>>>(bt);
+        if (lean) sparsify_grouped_nm_batched_kernel<bf16_t, 1><<<grid, kSpBatchThreads, 0, st>>>(bt);
+        else sparsify_grouped_nm_batched_kernel<bf16_t, 0><<<grid, kSpBatchThreads, 0, st>>>(bt);
     }
     return last_cuda();
 }
