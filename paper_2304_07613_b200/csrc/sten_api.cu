@@ -57,7 +57,8 @@ inline unsigned grid1d(int64_t threads) { return unsigned((threads + 255) / 256)
 template <typename T, int MB, int NK>
 void launch_sparsify_nk(const void* W, int64_t ldw, int64_t G, int64_t KB, sten_nmg f, void* values,
                         int64_t Kp, uint8_t* idx, int aligned, cudaStream_t st) {
-    sparsify_grouped_nm_kernel<T, MB, NK><<<grid1d(G * KB), 256, 0, st>>>(
+    sparsify_grouped_nm_kernel<T, MB, NK><<<unsigned((G * KB + kSpBatchThreads - 1) / kSpBatchThreads),
+                                            kSpBatchThreads, 0, st>>>(
         static_cast<const T*>(W), ldw, G, KB, f.n, f.g, static_cast<T*>(values), Kp, idx, aligned);
 }
 
